@@ -1,0 +1,89 @@
+/* qoq_oracle.h — CPU oracle for the QoQ W4A8 hot path of QServe (arXiv 2405.04532).
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library. The product path (include/qoq_b200.h,
+ * paper_2405_04532_b200/) never includes, links or calls anything here, and this oracle
+ * shares no code, header, table or constant generator with it.
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX source, with its section/equation.
+ * Readings of silent/ambiguous passages are numbered Q1..Q19 as in DESIGN.md §3.
+ *
+ * fp16 values are carried as raw IEEE binary16 bit patterns (uint16_t).
+ * All functions return 0 on success, a negative value on a precondition failure.
+ */
+#ifndef QOQ_ORACLE_H
+#define QOQ_ORACLE_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* IEEE binary16 <-> binary32. f2h rounds to nearest, ties to even (Q8, Q10). */
+float    oracle_h2f(uint16_t h);
+uint16_t oracle_f2h_rn(float f);
+
+/* Round half away from zero of the integer quotient a/b, b > 0 (Q1: the paper's ⌈·⌋). */
+int      oracle_rhai(int a, int b);
+
+/* O1 — level-1 progressive quantization, per output channel, symmetric INT8 into the
+ * protective range [-119, 119]. Eq. (progressive_quant:int8); range P:257-275.
+ * W: [N][K] fp16 (nn.Linear layout, Q9). q8: [N][K] int8 out. s0: [N] fp16 out. */
+int oracle_level1(const uint16_t* W, int N, int K, int8_t* q8, uint16_t* s0);
+
+/* O2 — level-2 progressive quantization of ONE group of g level-1 codes: per-group
+ * asymmetric UINT4 with an unsigned 8-bit integer scale. Eq. (progressive_quant:int4)
+ * P:247-253 with Eq. 2 at q_min = 0, q_max = 15; worked example P:257.
+ * Writes qu4[g] in [0,15], *s_u8 >= 1, *z in [0,15]. */
+int oracle_level2_group(const int8_t* q8, int g, uint8_t* qu4, uint8_t* s_u8, uint8_t* z);
+
+/* O2 over a whole [N][K] level-1 tensor, group size g along K.
+ * qu4: [N][K]; s_u8, z: [N][K/g]. */
+int oracle_level2(const int8_t* q8, int N, int K, int g, uint8_t* qu4, uint8_t* s_u8, uint8_t* z);
+
+/* Level-2 dequantization, Eq. (progressive_quant:int4) read right to left:
+ * qhat[n][k] = (qu4 - z) * s_u8 (exact integer, may exceed INT8 only if the protective
+ * range is violated). qhat is int16 so an overflow is observable. */
+int oracle_dequant_level2(const uint8_t* qu4, const uint8_t* s_u8, const uint8_t* z,
+                          int N, int K, int g, int16_t* qhat);
+
+/* O3 — pack into the frozen tile stream (DESIGN.md §4 "Packed weight layout"; the B200 form
+ * of "store the weights in the order they are used", with the RLP nibble interleave
+ * w0,w16,w1,w17,... of P:447, reading Q15). 128x128 tiles of 8448 bytes, n-tile-major.
+ * packed must hold (N/128)*(K/128)*8448 bytes. Requires g == 128, N%128 == K%128 == 0. */
+int oracle_pack(const uint8_t* qu4, const uint8_t* s_u8, const uint8_t* z, int N, int K, int g,
+                uint8_t* packed);
+/* Inverse of oracle_pack. */
+int oracle_unpack(const uint8_t* packed, int N, int K, int g,
+                  uint8_t* qu4, uint8_t* s_u8, uint8_t* z);
+
+/* O4 — per-token symmetric INT8 activation quantization (§6.1; symmetric form P:132).
+ * X: [M][ldx] fp16. qx: [M][K] int8; sx: [M] fp16; tx: [M] int32 row sums of qx (nullable). */
+int oracle_quantize_activations(const uint16_t* X, int M, int K, int ldx,
+                                int8_t* qx, uint16_t* sx, int32_t* tx);
+
+/* O5 — integer GEMM: acc[m][n] = sum_k qx[m][k] * qhat[n][k], accumulated in int64 and
+ * checked to fit INT32 ("INT32 partial sums", "INT8 matrix multiplication as if it
+ * was W8A8"). Returns -2 if any result leaves the int32 range. Rows [m0, m1) only. */
+int oracle_gemm_i32(const int8_t* qx, const int16_t* qhat, int M, int N, int K,
+                    int m0, int m1, int32_t* acc);
+
+/* O6 — epilogue reference y = acc * s_x[m] * s0[n] in fp64 (the s_W x s_X outer
+ * product scaling in the epilogue). Exact in fp64 (<= 51 significant bits). */
+int oracle_epilogue_f64(const int32_t* acc, const uint16_t* sx, const uint16_t* s0,
+                        int M, int N, double* y);
+
+/* The whole linear layer from packed weights, rows [m0, m1) of X only (used for sampled
+ * parity at full size and for the timed CPU baseline): O4 on those rows -> unpack (O3^-1) ->
+ * dequant level 2 -> O5 -> O6. y: [(m1-m0)][N]. qhat_scratch: N*K int16 or NULL (allocated). */
+int oracle_linear_rows(const uint16_t* X, int K, int ldx, int m0, int m1,
+                       const uint8_t* packed, const uint16_t* s0, int N, double* y);
+
+/* Number of OpenMP threads the oracle's parallel loops use (1 without OpenMP). */
+int oracle_num_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
