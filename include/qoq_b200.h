@@ -1,0 +1,123 @@
+/* qoq_b200.h — C ABI of the B200-native (sm_100a) QoQ W4A8 hot path of QServe (arXiv 2405.04532).
+ *
+ * The problem statement this library implements, PAPER.md P:407 (§5.1): "All GEMM layers in
+ * QServe operate on W4A8 inputs, perform computation on INT8 tensor cores, and generate FP16
+ * outputs." Weights are progressively group-quantized (§4.1; g = 128 per P:814);
+ * activations are quantized per token, symmetric INT8 (§6.1).
+ *
+ * Conventions (every entry point):
+ *   - Pointers are DEVICE pointers unless the name ends in _host. All buffers are caller-owned;
+ *     the library never allocates, never synchronizes the device, and keeps no mutable global
+ *     state. Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   - fp16 buffers are IEEE binary16 (void* to stay free of CUDA headers).
+ *   - Arguments are validated on the host, synchronously; on failure nothing is launched and a
+ *     qoq_status != QOQ_OK is returned. A launch failure returns QOQ_ERR_CUDA. Faults inside a
+ *     kernel surface as CUDA errors at the caller's next synchronization. Nothing throws.
+ *   - Device buffers must be 16-byte aligned. Requires an sm_100 device (else QOQ_ERR_ARCH).
+ *   - Inputs containing NaN/Inf are a precondition violation (results unspecified).
+ */
+#ifndef QOQ_B200_H
+#define QOQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    QOQ_OK = 0,
+    QOQ_ERR_INVALID_ARG = 1,  /* null pointer, misalignment, negative size, ldx < K, ...      */
+    QOQ_ERR_SHAPE = 2,        /* N or K not a multiple of 128, K too large for INT32 headroom */
+    QOQ_ERR_UNSUPPORTED = 3,  /* group != 128                                                 */
+    QOQ_ERR_ARCH = 4,         /* current device is not sm_100                                 */
+    QOQ_ERR_WORKSPACE = 5,    /* workspace / packed buffer smaller than required             */
+    QOQ_ERR_CUDA = 6          /* a CUDA runtime call or kernel launch failed                 */
+} qoq_status;
+
+/* Static description of a status code; never NULL. */
+const char* qoq_status_string(int status);
+/* ABI version of this header (incremented on any signature or layout change). */
+int qoq_abi_version(void);
+#define QOQ_ABI_VERSION 1
+
+/* ----------------------------------------------------------------------------------------------
+ * Packed weight layout (frozen). The B200 form of "store the weights in the order
+ * they are used during computation" (§5.2.1) with the register-level-parallel nibble
+ * interleave w0,w16,w1,w17,... (§5.2.2, Fig. 9):
+ *   tiles of 128 output channels x 128 input channels (= one group), n-tile-major:
+ *   tile(nt, j) starts at byte (nt*(K/128) + j) * 8448;
+ *   bytes [0, 8192): q_u4; chunk c = 0..3 covers k = 128j+32c .. +31; row r (0..127) of chunk c
+ *                    is at c*2048 + r*16; byte b (0..15) = q[r][32c+b] | q[r][32c+16+b] << 4;
+ *   bytes [8192, 8320): s_u8[r]       (level-2 group scale)
+ *   bytes [8320, 8448): zs_u8[r] = z_u4 * s_u8  (precomputed zero term; <= 126 by the
+ *                                   protective range)
+ * -------------------------------------------------------------------------------------------- */
+
+/* Bytes of the packed weight stream for an [N][K] weight; 0 if the shape is unsupported
+ * (group != 128, N or K not a positive multiple of 128). */
+size_t qoq_packed_weight_bytes(int N, int K, int group);
+
+/* Offline weight quantization + packing (P:238-275 levels 1 and 2; P:434/P:447 layout).
+ *   W        [N][K] fp16 row-major (nn.Linear layout: Y = X W^T).
+ *   packed   out, qoq_packed_weight_bytes(N,K,group) bytes (packed_bytes must be >= that).
+ *   s0_fp16  out, [N] level-1 per-channel scales s0 = fp16(max_k|W[n,k]| / 119).
+ * Level 1: q8 = clamp(round_half_away(W / s0), -119, 119) (protective range).
+ * Level 2 (per 128-group): s_u8 = max(1, ⌈(hi-lo)/15⌋), z = clamp(⌈-lo/s_u8⌋, 0, 15),
+ *          q_u4 = clamp(⌈(q8 + z s_u8)/s_u8⌋, 0, 15) (Eq. 2 P:111-116 with q_min=0, q_max=15). */
+int qoq_quantize_weights(const void* W_fp16, int N, int K, int group,
+                         void* packed, size_t packed_bytes, void* s0_fp16, void* stream);
+
+/* Per-token symmetric INT8 activation quantization (symmetric form P:132).
+ *   X_fp16  [M][ldx] fp16 (ldx >= K, ldx % 8 == 0; lets a TP rank quantize a K-shard view).
+ *   qx      out [M][K] int8 (contiguous), q = clamp(round_half_away(x / s_x), -127, 127).
+ *   sx_fp16 out [M], s_x = fp16(max_k|X[m,k]| / 127); 1.0 for an all-zero row.
+ *   tx      out [M] int32 row sums Σ_k qx (nullable). Lets the GEMM feed biased-u8 weights.
+ * Requires K % 8 == 0. M == 0 is a no-op. */
+int qoq_quantize_activations_per_token(const void* X_fp16, int M, int K, int ldx,
+                                       int8_t* qx, void* sx_fp16, int32_t* tx, void* stream);
+
+/* Scratch needed by qoq_w4a8_gemm / qoq_w4a8_gemm_i32 for this shape (split-K INT32 partials and
+ * per-tile arrival counters). The workspace must be ZERO-FILLED before its first use; every
+ * successful call leaves it zero-filled again. One workspace per concurrently running stream. */
+size_t qoq_gemm_workspace_bytes(int M, int N, int K);
+
+/* The W4A8 per-group GEMM with progressive dequantization (§5.2):
+ *   Y[m][n] = fp16( s_x[m] * s0[n] * Σ_k qx[m][k] * q̂[n][k] ),  q̂ = (q_u4 - z) * s_u8 ∈ INT8,
+ * with q_u4 expanded to INT8 in registers, contracted on tcgen05 INT8 tensor
+ * cores with INT32 accumulation in tensor memory, scaled in the epilogue.
+ *   qx [M][K] int8, sx_fp16 [M], tx [M] int32 or NULL (if given, must equal Σ_k qx[m][k]).
+ *   packed / s0_fp16 from qoq_quantize_weights.  Y_fp16 [M][ldy], ldy >= N.
+ * Requires group == 128, N % 128 == 0, K % 128 == 0, K <= 65536. M == 0 is a no-op. */
+int qoq_w4a8_gemm(const int8_t* qx, const void* sx_fp16, const int32_t* tx,
+                  const void* packed, const void* s0_fp16,
+                  int M, int N, int K, int group,
+                  void* Y_fp16, int ldy,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* Parity/debug entry: the same main loop; the epilogue writes the exact INT32 accumulators
+ * acc[m][n] = Σ_k qx[m][k] * q̂[n][k] (bias-corrected) into acc [M][ldacc] instead of Y. */
+int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed,
+                      int M, int N, int K, int group,
+                      int32_t* acc, int ldacc,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* End-to-end linear layer with HOST activations (the e2e measurement path): copies X_host
+ * (pinned host memory, [M][K] fp16) to the device, quantizes it per token, runs the W4A8 GEMM
+ * against device-resident packed weights and copies Y back to Y_host ([M][N] fp16, pinned).
+ * dev_scratch: qoq_linear_host_scratch_bytes(M,N,K) bytes of device memory, zero-filled
+ * before first use (it embeds the GEMM workspace). Asynchronous on `stream`. */
+size_t qoq_linear_host_scratch_bytes(int M, int N, int K);
+int qoq_linear_host(const void* X_host_fp16, int M, int K,
+                    const void* packed, const void* s0_fp16, int N,
+                    void* Y_host_fp16, void* dev_scratch, size_t scratch_bytes, void* stream);
+
+/* Kernels launched per successful call (launch accounting for benchmarks):
+ * quantize_weights 2, quantize_activations_per_token 1, w4a8_gemm 1, w4a8_gemm_i32 1,
+ * linear_host 2 (plus 2 async copies). */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QOQ_B200_H */

@@ -1,0 +1,204 @@
+"""B200-native (sm_100a) QoQ W4A8 hot path of QServe (arXiv 2405.04532) — Python binding.
+
+Thin ctypes marshalling over the C ABI in include/qoq_b200.h (libqoq_b200.so, built in-tree):
+every step of the path runs in the library's CUDA kernels. PyTorch is used only for device memory,
+streams and process groups. There is no CPU fallback: if the library or an sm_100 GPU is missing,
+every call raises.
+
+Function names follow the ABI: quantize_weights, quantize_activations_per_token, w4a8_gemm,
+w4a8_gemm_i32, linear_host. Tensors are torch tensors on the current CUDA device; calls are
+asynchronous on torch's current stream (or `stream=`).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqoq_b200.so")
+GROUP = 128
+TILE_BYTES = 8448
+ABI_VERSION = 1
+# kernels launched per call (matches include/qoq_b200.h)
+LAUNCHES = {"quantize_weights": 2, "quantize_activations_per_token": 1, "w4a8_gemm": 1,
+            "w4a8_gemm_i32": 1, "linear_host": 2}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class QoQError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn}: status {status} ({msg})")
+        self.status = status
+
+
+def load() -> ctypes.CDLL:
+    """Load libqoq_b200.so (raises if it was not built — no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not found: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I, Z = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+        sig = {
+            "qoq_status_string": (ctypes.c_char_p, [I]),
+            "qoq_abi_version": (I, []),
+            "qoq_packed_weight_bytes": (Z, [I, I, I]),
+            "qoq_quantize_weights": (I, [P, I, I, I, P, Z, P, P]),
+            "qoq_quantize_activations_per_token": (I, [P, I, I, I, P, P, P, P]),
+            "qoq_gemm_workspace_bytes": (Z, [I, I, I]),
+            "qoq_w4a8_gemm": (I, [P, P, P, P, P, I, I, I, I, P, I, P, Z, P]),
+            "qoq_w4a8_gemm_i32": (I, [P, P, P, I, I, I, I, P, I, P, Z, P]),
+            "qoq_linear_host_scratch_bytes": (Z, [I, I, I]),
+            "qoq_linear_host": (I, [P, I, I, P, P, I, P, P, Z, P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        if L.qoq_abi_version() != ABI_VERSION:
+            raise ImportError("libqoq_b200.so ABI version mismatch; rebuild")
+        _lib = L
+    return _lib
+
+
+def _check(fn: str, rc: int):
+    if rc != 0:
+        raise QoQError(fn, rc, load().qoq_status_string(rc).decode())
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+# ------------------------------------------------------------------ sizes
+
+def packed_weight_bytes(N: int, K: int, group: int = GROUP) -> int:
+    return load().qoq_packed_weight_bytes(N, K, group)
+
+
+def gemm_workspace_bytes(M: int, N: int, K: int) -> int:
+    return load().qoq_gemm_workspace_bytes(M, N, K)
+
+
+def linear_host_scratch_bytes(M: int, N: int, K: int) -> int:
+    return load().qoq_linear_host_scratch_bytes(M, N, K)
+
+
+# ------------------------------------------------------------------ the three calls + debug
+
+def quantize_weights(W: torch.Tensor, group: int = GROUP, stream=None):
+    """W [N][K] fp16 (cuda) -> (packed uint8 tile stream, s0 fp16 [N])."""
+    if W.dtype != torch.float16 or W.dim() != 2:
+        raise ValueError("W must be a 2-D fp16 tensor")
+    N, K = W.shape
+    nbytes = packed_weight_bytes(N, K, group)
+    packed = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=W.device)
+    s0 = torch.empty(N, dtype=torch.float16, device=W.device)
+    _check("qoq_quantize_weights",
+           load().qoq_quantize_weights(_ptr(W), N, K, group, _ptr(packed), nbytes, _ptr(s0), _stream(stream)))
+    return packed[:nbytes], s0
+
+
+def quantize_activations_per_token(X: torch.Tensor, K: int | None = None, want_tx: bool = True,
+                                   out=None, stream=None):
+    """X [M][ldx] fp16 -> (qx int8 [M][K], sx fp16 [M], tx int32 [M] or None)."""
+    if X.dtype != torch.float16 or X.dim() != 2:
+        raise ValueError("X must be a 2-D fp16 tensor")
+    M, ldx = X.shape
+    K = ldx if K is None else K
+    if out is None:
+        qx = torch.empty(M, K, dtype=torch.int8, device=X.device)
+        sx = torch.empty(M, dtype=torch.float16, device=X.device)
+        tx = torch.empty(M, dtype=torch.int32, device=X.device) if want_tx else None
+    else:
+        qx, sx, tx = out
+    _check("qoq_quantize_activations_per_token",
+           load().qoq_quantize_activations_per_token(_ptr(X), M, K, ldx, _ptr(qx), _ptr(sx), _ptr(tx),
+                                                     _stream(stream)))
+    return qx, sx, tx
+
+
+class Workspace:
+    """Zero-filled GEMM workspace that grows on demand (the library leaves it zeroed)."""
+
+    def __init__(self, device=None):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int):
+        if nbytes == 0:
+            return None, 0
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device or "cuda")
+        return self.buf, self.buf.numel()
+
+
+_default_ws: dict = {}
+
+
+def _ws_for(device, nbytes, workspace):
+    if workspace is None:
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+        workspace = _default_ws.setdefault(key, Workspace(device))
+    return workspace.get(nbytes)
+
+
+def w4a8_gemm(qx: torch.Tensor, sx: torch.Tensor, tx: torch.Tensor | None, packed: torch.Tensor,
+              s0: torch.Tensor, N: int, out: torch.Tensor | None = None, workspace: Workspace | None = None,
+              stream=None) -> torch.Tensor:
+    """Y [M][N] fp16 = fp16(s_x[m] s0[n] Σ_k qx[m][k] q̂[n][k])."""
+    M, K = qx.shape
+    Y = torch.empty(M, N, dtype=torch.float16, device=qx.device) if out is None else out
+    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace)
+    _check("qoq_w4a8_gemm",
+           load().qoq_w4a8_gemm(_ptr(qx), _ptr(sx), _ptr(tx), _ptr(packed), _ptr(s0), M, N, K, GROUP,
+                                _ptr(Y), Y.stride(0), _ptr(ws), wsb, _stream(stream)))
+    return Y
+
+
+def w4a8_gemm_i32(qx: torch.Tensor, tx: torch.Tensor | None, packed: torch.Tensor, N: int,
+                  workspace: Workspace | None = None, stream=None) -> torch.Tensor:
+    """Exact INT32 accumulators acc [M][N] (parity/debug entry)."""
+    M, K = qx.shape
+    acc = torch.empty(M, N, dtype=torch.int32, device=qx.device)
+    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace)
+    _check("qoq_w4a8_gemm_i32",
+           load().qoq_w4a8_gemm_i32(_ptr(qx), _ptr(tx), _ptr(packed), M, N, K, GROUP, _ptr(acc), N,
+                                    _ptr(ws), wsb, _stream(stream)))
+    return acc
+
+
+def linear(X: torch.Tensor, packed: torch.Tensor, s0: torch.Tensor, N: int, K: int | None = None,
+           workspace: Workspace | None = None, stream=None) -> torch.Tensor:
+    """Quantize X per token, then W4A8 GEMM (two kernels, chained with PDL)."""
+    qx, sx, tx = quantize_activations_per_token(X, K, stream=stream)
+    return w4a8_gemm(qx, sx, tx, packed, s0, N, workspace=workspace, stream=stream)
+
+
+def linear_host(X_host: torch.Tensor, packed: torch.Tensor, s0: torch.Tensor, N: int,
+                Y_host: torch.Tensor, scratch: torch.Tensor, stream=None):
+    """End-to-end through the C ABI with pinned HOST X/Y: H2D, quantize, GEMM, D2H (async)."""
+    if X_host.is_cuda or Y_host.is_cuda:
+        raise ValueError("linear_host takes host tensors")
+    M, K = X_host.shape
+    _check("qoq_linear_host",
+           load().qoq_linear_host(ctypes.c_void_p(X_host.data_ptr()), M, K, _ptr(packed), _ptr(s0), N,
+                                  ctypes.c_void_p(Y_host.data_ptr()), _ptr(scratch), scratch.numel(),
+                                  _stream(stream)))

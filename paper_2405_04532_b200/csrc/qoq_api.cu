@@ -1,0 +1,162 @@
+// qoq_api.cu — the C-ABI shim (include/qoq_b200.h): host-side validation, planning and launch.
+// No allocation, no device synchronization, no mutable global state (a resolved driver entry
+// point is cached in w4a8_gemm.cu).
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/qoq_b200.h"
+#include "qoq_internal.h"
+
+namespace {
+
+using namespace qoq;
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int check_arch(int* num_sms) {
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return QOQ_ERR_CUDA;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+        return QOQ_ERR_CUDA;
+    if (major != 10 || minor != 0) return QOQ_ERR_ARCH;
+    if (num_sms && cudaDeviceGetAttribute(num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return QOQ_ERR_CUDA;
+    return QOQ_OK;
+}
+
+int gemm_shape_status(int M, int N, int K, int group) {
+    if (M < 0 || N <= 0 || K <= 0) return QOQ_ERR_INVALID_ARG;
+    if (group != 128) return QOQ_ERR_UNSUPPORTED;
+    if (N % kTileN != 0 || K % kTileK != 0) return QOQ_ERR_SHAPE;
+    if (K > 65536) return QOQ_ERR_SHAPE;   // INT32 headroom of the biased-u8 accumulation
+    return QOQ_OK;
+}
+
+int num_sms_or_default() {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+}
+
+int run_gemm(const int8_t* qx, const void* sx, const int32_t* tx, const void* packed, const void* s0,
+             int M, int N, int K, int group, void* out, int ldo, bool out_i32,
+             void* ws, size_t ws_bytes, cudaStream_t st) {
+    int rc = gemm_shape_status(M, N, K, group);
+    if (rc) return rc;
+    if (M == 0) return QOQ_OK;
+    if (!qx || !packed || !out || (!out_i32 && (!sx || !s0))) return QOQ_ERR_INVALID_ARG;
+    if (!aligned16(qx) || !aligned16(packed) || ldo < N) return QOQ_ERR_INVALID_ARG;
+    int sms = 0;
+    if ((rc = check_arch(&sms))) return rc;
+    GemmPlan p = plan_gemm(M, N, K, sms);
+    if (p.ws_bytes > 0 && (!ws || ws_bytes < p.ws_bytes || !aligned16(ws))) return QOQ_ERR_WORKSPACE;
+    GemmArgs a{qx, sx, tx, packed, s0, out, ldo, out_i32, M, N, K, p.ws_bytes ? ws : nullptr};
+    return launch_w4a8_gemm(a, p, st, /*pdl=*/true) == cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" {
+
+const char* qoq_status_string(int s) {
+    switch (s) {
+        case QOQ_OK: return "ok";
+        case QOQ_ERR_INVALID_ARG: return "invalid argument";
+        case QOQ_ERR_SHAPE: return "unsupported shape (N, K must be multiples of 128; K <= 65536)";
+        case QOQ_ERR_UNSUPPORTED: return "unsupported configuration (group must be 128)";
+        case QOQ_ERR_ARCH: return "device is not sm_100 (B200)";
+        case QOQ_ERR_WORKSPACE: return "workspace or output buffer too small";
+        case QOQ_ERR_CUDA: return "CUDA error";
+        default: return "unknown status";
+    }
+}
+
+int qoq_abi_version(void) { return QOQ_ABI_VERSION; }
+
+size_t qoq_packed_weight_bytes(int N, int K, int group) {
+    if (group != 128 || N <= 0 || K <= 0 || N % kTileN || K % kTileK) return 0;
+    return (size_t)(N / kTileN) * (size_t)(K / kTileK) * kTileBytes;
+}
+
+int qoq_quantize_weights(const void* W, int N, int K, int group, void* packed, size_t packed_bytes, void* s0,
+                         void* stream) {
+    if (group != 128) return QOQ_ERR_UNSUPPORTED;
+    if (N <= 0 || K <= 0) return QOQ_ERR_INVALID_ARG;
+    if (N % kTileN || K % kTileK) return QOQ_ERR_SHAPE;
+    if (!W || !packed || !s0 || !aligned16(W) || !aligned16(packed)) return QOQ_ERR_INVALID_ARG;
+    if (packed_bytes < qoq_packed_weight_bytes(N, K, group)) return QOQ_ERR_WORKSPACE;
+    int rc = check_arch(nullptr);
+    if (rc) return rc;
+    return launch_quantize_weights(W, N, K, packed, s0, static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
+int qoq_quantize_activations_per_token(const void* X, int M, int K, int ldx, int8_t* qx, void* sx, int32_t* tx,
+                                       void* stream) {
+    if (M < 0 || K <= 0 || ldx < K) return QOQ_ERR_INVALID_ARG;
+    if (K % 8 || ldx % 8) return QOQ_ERR_SHAPE;
+    if (M == 0) return QOQ_OK;
+    if (!X || !qx || !sx || !aligned16(X) || (reinterpret_cast<uintptr_t>(qx) & 7u)) return QOQ_ERR_INVALID_ARG;
+    int rc = check_arch(nullptr);
+    if (rc) return rc;
+    return launch_quantize_activations(X, M, K, ldx, qx, sx, tx, static_cast<cudaStream_t>(stream), true) ==
+                   cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
+size_t qoq_gemm_workspace_bytes(int M, int N, int K) {
+    if (gemm_shape_status(M, N, K, 128) != QOQ_OK || M == 0) return 0;
+    return plan_gemm(M, N, K, num_sms_or_default()).ws_bytes;
+}
+
+int qoq_w4a8_gemm(const int8_t* qx, const void* sx, const int32_t* tx, const void* packed, const void* s0, int M,
+                  int N, int K, int group, void* Y, int ldy, void* ws, size_t ws_bytes, void* stream) {
+    if (ldy < N) return QOQ_ERR_INVALID_ARG;
+    return run_gemm(qx, sx, tx, packed, s0, M, N, K, group, Y, ldy, false, ws, ws_bytes,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed, int M, int N, int K, int group,
+                      int32_t* acc, int ldacc, void* ws, size_t ws_bytes, void* stream) {
+    if (ldacc < N) return QOQ_ERR_INVALID_ARG;
+    return run_gemm(qx, nullptr, tx, packed, nullptr, M, N, K, group, acc, ldacc, true, ws, ws_bytes,
+                    static_cast<cudaStream_t>(stream));
+}
+
+// scratch layout: [X fp16 M*K][qx M*K][sx 2M][tx 4M][Y fp16 M*N][gemm workspace], each 256-B aligned
+size_t qoq_linear_host_scratch_bytes(int M, int N, int K) {
+    if (gemm_shape_status(M, N, K, 128) != QOQ_OK) return 0;
+    size_t b = align_up((size_t)M * K * 2, 256) + align_up((size_t)M * K, 256) + align_up((size_t)M * 2, 256) +
+               align_up((size_t)M * 4, 256) + align_up((size_t)M * N * 2, 256);
+    return b + align_up(qoq_gemm_workspace_bytes(M, N, K), 256);
+}
+
+int qoq_linear_host(const void* X_host, int M, int K, const void* packed, const void* s0, int N, void* Y_host,
+                    void* scratch, size_t scratch_bytes, void* stream) {
+    int rc = gemm_shape_status(M, N, K, 128);
+    if (rc) return rc;
+    if (M == 0) return QOQ_OK;
+    if (!X_host || !Y_host || !packed || !s0 || !scratch || !aligned16(scratch)) return QOQ_ERR_INVALID_ARG;
+    if (scratch_bytes < qoq_linear_host_scratch_bytes(M, N, K)) return QOQ_ERR_WORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* b = static_cast<uint8_t*>(scratch);
+    void* Xd = b;                b += align_up((size_t)M * K * 2, 256);
+    int8_t* qx = (int8_t*)b;     b += align_up((size_t)M * K, 256);
+    void* sx = b;                b += align_up((size_t)M * 2, 256);
+    int32_t* tx = (int32_t*)b;   b += align_up((size_t)M * 4, 256);
+    void* Yd = b;                b += align_up((size_t)M * N * 2, 256);
+    void* ws = b;
+    if (cudaMemcpyAsync(Xd, X_host, (size_t)M * K * 2, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return QOQ_ERR_CUDA;
+    if ((rc = qoq_quantize_activations_per_token(Xd, M, K, K, qx, sx, tx, stream))) return rc;
+    if ((rc = qoq_w4a8_gemm(qx, sx, tx, packed, s0, M, N, K, 128, Yd, N, ws, qoq_gemm_workspace_bytes(M, N, K),
+                            stream)))
+        return rc;
+    if (cudaMemcpyAsync(Y_host, Yd, (size_t)M * N * 2, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return QOQ_ERR_CUDA;
+    return QOQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// qoq_internal.h — host-side declarations shared by the C-ABI shim (qoq_api.cu) and the kernel
+// translation units. Not part of the public ABI (that is include/qoq_b200.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace qoq {
+
+constexpr int kTileN = 128;          // output channels per packed tile (MMA M)
+constexpr int kTileK = 128;          // input channels per packed tile (= group size g)
+constexpr int kTileBytes = 8448;     // 8192 B of u4 codes + 128 B s_u8 + 128 B z*s_u8
+
+// Work decomposition of one GEMM launch (host planner <-> kernel scheduler).
+struct GemmPlan {
+    int BN;          // token tile = MMA N (16, 32, 64, 128 or 256)
+    int MT, NT, KT;  // token tiles, 128-row weight tiles, 128-deep K tiles
+    int T;           // output tiles = MT * NT
+    long long I;     // k-iterations = T * KT
+    int G;           // CTAs (persistent, <= #SMs)
+    int mode;        // 0: whole tiles round-robin; 1: contiguous k-iteration ranges (split-K)
+    size_t ws_bytes; // INT32 partials + per-tile counters (mode 1), else 0
+};
+
+GemmPlan plan_gemm(int M, int N, int K, int num_sms);
+
+struct GemmArgs {
+    const int8_t* qx;
+    const void* sx;
+    const int32_t* tx;
+    const void* packed;
+    const void* s0;
+    void* out;       // fp16 Y or int32 acc
+    int ldo;
+    bool out_i32;
+    int M, N, K;
+    void* ws;
+};
+
+cudaError_t launch_w4a8_gemm(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl);
+cudaError_t launch_quantize_weights(const void* W, int N, int K, void* packed, void* s0, cudaStream_t st);
+cudaError_t launch_quantize_activations(const void* X, int M, int K, int ldx, int8_t* qx, void* sx,
+                                        int32_t* tx, cudaStream_t st, bool pdl);
+
+}  // namespace qoq

@@ -1,0 +1,209 @@
+// quantize.cu — the two quantizers of the QoQ W4A8 hot path (sm_100a).
+//
+//  * Offline weight quantization + packing (§4.1 progressive group quantization;
+//    layout P:434/P:447, frozen in include/qoq_b200.h):
+//      level1_scale_kernel : s0[n] = fp16(max_k |W[n,k]| / 119)
+//      level2_pack_kernel  : q8 = clamp(⌈W/s0⌋, ±119) -> per-group u8 scale, u4 zero, u4 codes
+//                            -> packed 128x128 tile stream
+//  * Per-token symmetric INT8 activation quantization, bandwidth-bound:
+//      quantize_act_kernel : s_x[m] = fp16(max_k|X[m,k]| / 127), q = clamp(⌈X/s_x⌋, ±127),
+//                            t_x[m] = Σ_k q (feeds the biased-u8 GEMM epilogue)
+//
+// Floating-point decisions use IEEE fp32 division (no fast-math), round-half-away (roundf) and
+// __float2half_rn, so the codes are deterministic functions of the fp16 inputs.
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "qoq_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace qoq {
+
+__device__ __forceinline__ float block_reduce_max(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    v = (l < nw) ? red[l] : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;  // valid in every thread
+}
+
+__device__ __forceinline__ int block_reduce_sum(int v, int* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    v = (l < nw) ? red[l] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Symmetric fp16 scale: fp16_rn(amax / qmax); 1.0 for amax == 0; 2^-24 if it underflows to 0.
+__device__ __forceinline__ __half sym_scale(float amax, float qmax) {
+    if (amax == 0.0f) return __float2half_rn(1.0f);
+    __half s = __float2half_rn(__fdiv_rn(amax, qmax));
+    if ((__half_as_ushort(s) & 0x7fff) == 0) s = __ushort_as_half(1);
+    return s;
+}
+
+__device__ __forceinline__ float amax8(uint4 v, float a) {
+    const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 f = __half22float2(h[i]);
+        a = fmaxf(a, fmaxf(fabsf(f.x), fabsf(f.y)));
+    }
+    return a;
+}
+
+// ------------------------------------------------------------------ weights, level 1
+
+__global__ void __launch_bounds__(256) level1_scale_kernel(const __half* __restrict__ W, int K,
+                                                           __half* __restrict__ s0) {
+    __shared__ float red[32];
+    pdl_wait();
+    const uint4* row = reinterpret_cast<const uint4*>(W + (size_t)blockIdx.x * K);
+    float a = 0.0f;
+    for (int i = threadIdx.x; i < K / 8; i += blockDim.x) a = amax8(__ldg(row + i), a);
+    a = block_reduce_max(a, red);
+    if (threadIdx.x == 0) s0[blockIdx.x] = sym_scale(a, 119.0f);
+}
+
+// round half away from zero of a/b for integers, b > 0 (the paper's ⌈·⌋ on integers)
+__device__ __forceinline__ int rhai(int a, int b) {
+    const int m = a < 0 ? -a : a;
+    const int q = (2 * m + b) / (2 * b);
+    return a < 0 ? -q : q;
+}
+
+__device__ __forceinline__ int q8_of(__half w, float s) {
+    const int q = (int)roundf(__fdiv_rn(__half2float(w), s));
+    return min(119, max(-119, q));
+}
+
+// grid (K/128, N/128), 128 threads: thread r owns output channel n = 128*blockIdx.y + r of
+// group j = blockIdx.x and writes its 4 x 16 B of codes in the consumption order of the GEMM.
+__global__ void __launch_bounds__(128) level2_pack_kernel(const __half* __restrict__ W, int K,
+                                                          const __half* __restrict__ s0,
+                                                          uint8_t* __restrict__ packed) {
+    pdl_wait();
+    const int j = blockIdx.x, nt = blockIdx.y, r = threadIdx.x;
+    const int n = nt * 128 + r, KT = K / 128;
+    const float s = __half2float(s0[n]);
+    const uint4* src = reinterpret_cast<const uint4*>(W + (size_t)n * K + (size_t)j * 128);
+    // pass 1: the group's level-1 code range
+    int lo = 127, hi = -127;
+#pragma unroll 4
+    for (int v = 0; v < 16; ++v) {
+        uint4 u = __ldg(src + v);
+        const __half* h = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int q = q8_of(h[e], s);
+            lo = min(lo, q);
+            hi = max(hi, q);
+        }
+    }
+    const int su = max(1, rhai(hi - lo, 15));
+    const int z = min(15, max(0, rhai(-lo, su)));
+    uint8_t* tile = packed + ((size_t)nt * KT + j) * 8448;
+    // pass 2: codes, packed as byte b = w_b | w_{b+16} << 4 within each 32-wide chunk
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+        int code[32];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            uint4 u = __ldg(src + c * 4 + v);
+            const __half* h = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) code[v * 8 + e] = min(15, max(0, rhai(q8_of(h[e], s) + z * su, su)));
+        }
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            w[i] = 0;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                const int b = 4 * i + bb;
+                w[i] |= (uint32_t)(code[b] | (code[b + 16] << 4)) << (8 * bb);
+            }
+        }
+        *reinterpret_cast<uint4*>(tile + c * 2048 + r * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    tile[8192 + r] = (uint8_t)su;
+    tile[8320 + r] = (uint8_t)(z * su);
+}
+
+// ------------------------------------------------------------------ activations
+
+__global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restrict__ X, int K, int ldx,
+                                                           int8_t* __restrict__ qx, __half* __restrict__ sx,
+                                                           int32_t* __restrict__ tx) {
+    __shared__ float redf[32];
+    __shared__ int redi[32];
+    pdl_wait();
+    const int m = blockIdx.x;
+    const uint4* row = reinterpret_cast<const uint4*>(X + (size_t)m * ldx);
+    const int nv = K / 8;
+    float a = 0.0f;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) a = amax8(__ldg(row + i), a);
+    a = block_reduce_max(a, redf);
+    const __half sh = sym_scale(a, 127.0f);
+    const float s = __half2float(sh);
+    int t = 0;
+    uint2* out = reinterpret_cast<uint2*>(qx + (size_t)m * K);
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        uint4 u = __ldg(row + i);
+        const __half* h = reinterpret_cast<const __half*>(&u);
+        uint32_t w[2] = {0, 0};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int q = min(127, max(-127, (int)roundf(__fdiv_rn(__half2float(h[e]), s))));
+            t += q;
+            w[e >> 2] |= (uint32_t)(q & 0xff) << (8 * (e & 3));
+        }
+        out[i] = make_uint2(w[0], w[1]);
+    }
+    pdl_launch_dependents();
+    if (tx) t = block_reduce_sum(t, redi);
+    if (threadIdx.x == 0) {
+        sx[m] = sh;
+        if (tx) tx[m] = t;
+    }
+}
+
+// ------------------------------------------------------------------ launchers
+
+cudaError_t launch_quantize_weights(const void* W, int N, int K, void* packed, void* s0, cudaStream_t st) {
+    level1_scale_kernel<<<N, 256, 0, st>>>(static_cast<const __half*>(W), K, static_cast<__half*>(s0));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    level2_pack_kernel<<<dim3(K / 128, N / 128), 128, 0, st>>>(static_cast<const __half*>(W), K,
+                                                                static_cast<const __half*>(s0),
+                                                                static_cast<uint8_t*>(packed));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quantize_activations(const void* X, int M, int K, int ldx, int8_t* qx, void* sx,
+                                        int32_t* tx, cudaStream_t st, bool pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(M);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, quantize_act_kernel, static_cast<const __half*>(X), K, ldx, qx,
+                              static_cast<__half*>(sx), tx);
+}
+
+}  // namespace qoq

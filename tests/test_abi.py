@@ -1,0 +1,75 @@
+"""C-ABI library: loads, exports every symbol include/qoq_b200.h declares, and validates arguments
+on the host (no compute calls — these run without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "qoq_b200.h")
+
+
+def declared_functions():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(qoq_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2405_04532_b200 import build
+    build.build()
+    import paper_2405_04532_b200 as qoq
+    return qoq.load()
+
+
+def test_header_declares_the_paper_calls():
+    fns = declared_functions()
+    for f in ("qoq_quantize_weights", "qoq_quantize_activations_per_token", "qoq_w4a8_gemm"):
+        assert f in fns
+
+
+def test_every_declared_symbol_is_exported(lib):
+    out = subprocess.check_output(["nm", "-D", "--defined-only", lib._name]).decode()
+    exported = set(re.findall(r"\bT (qoq_[a-z0-9_]+)", out))
+    missing = [f for f in declared_functions() if f not in exported]
+    assert not missing, missing
+
+
+def test_library_is_sm100a_only(lib):
+    out = subprocess.check_output(["cuobjdump", "--list-elf", lib._name]).decode()
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_103" not in out
+
+
+def test_status_strings_and_version(lib):
+    assert lib.qoq_abi_version() == 1
+    for s in range(0, 8):
+        assert lib.qoq_status_string(s)
+
+
+def test_sizes(lib):
+    assert lib.qoq_packed_weight_bytes(256, 256, 128) == 4 * 8448
+    assert lib.qoq_packed_weight_bytes(4096, 14336, 128) == 30_277_632
+    assert lib.qoq_packed_weight_bytes(100, 256, 128) == 0
+    assert lib.qoq_packed_weight_bytes(256, 256, 64) == 0
+    assert lib.qoq_gemm_workspace_bytes(16, 64, 256) == 0                     # N not a multiple of 128
+    assert lib.qoq_linear_host_scratch_bytes(16, 256, 256) >= 16 * 256 * 5
+
+
+def test_host_validation_before_any_device_work(lib):
+    P = ctypes.c_void_p
+    fake = P(1 << 20)
+    # group != 128 -> UNSUPPORTED; N % 128 -> SHAPE; ldx < K -> INVALID_ARG (all host-side)
+    assert lib.qoq_quantize_weights(fake, 256, 256, 64, fake, 0, fake, None) == 3
+    assert lib.qoq_quantize_weights(fake, 200, 256, 128, fake, 0, fake, None) == 2
+    assert lib.qoq_quantize_activations_per_token(fake, 4, 256, 128, fake, fake, None, None) == 1
+    assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 4, 256, 200, 128, fake, 256, None, 0, None) == 2
+    assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 4, 256, 256, 64, fake, 256, None, 0, None) == 3
+    assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 4, 256, 256, 128, fake, 100, None, 0, None) == 1
+    assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 4, 256, 131072, 128, fake, 256, None, 0, None) == 2
+    # M == 0 is a no-op that never touches the device
+    assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 0, 256, 256, 128, fake, 256, None, 0, None) == 0
+    assert lib.qoq_quantize_activations_per_token(fake, 0, 256, 256, fake, fake, None, None) == 0

@@ -1,0 +1,168 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bit-exact: packed weights, s0, q_x, s_x, t_x and INT32 accumulators. FP16 Y within the north_star
+tolerance |Y - y_ref| <= 2e-3 |y_ref| + 1e-3, y_ref the exact fp64 oracle value."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 2e-3, 1e-3
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
+
+
+def bits16(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def check_y(Y, y_ref):
+    y = Y.cpu().numpy().astype(np.float64)
+    err = np.abs(y - y_ref)
+    bad = err > RTOL * np.abs(y_ref) + ATOL
+    assert not bad.any(), f"{bad.sum()} outputs outside tolerance; max err {err.max()}"
+
+
+# ------------------------------------------------------------------ weights
+
+@pytest.mark.parametrize("N,K", [(256, 256), (128, 128), (1280, 1024), (384, 4096)])
+def test_quantize_weights_bit_exact(gpu_lib, N, K):
+    W = synth.weights_fp16(N, K, seed=N + K)
+    W[3] = 0                                   # zero row -> s0 = 1
+    W[5] = np.float16(3e-7) * np.sign(W[5])    # underflowing row -> 2^-24 rule, clamp engaged
+    W[7, :128] = np.abs(W[7, :128])            # an all-positive group (the Q4 corner)
+    packed, s0 = gpu_lib.quantize_weights(to_dev(W))
+    p_ref, s0_ref = oracle.quantize_weights(W)
+    assert np.array_equal(bits16(s0), s0_ref.view(np.uint16))
+    assert np.array_equal(packed.cpu().numpy(), p_ref)
+
+
+# ------------------------------------------------------------------ activations
+
+@pytest.mark.parametrize("M,K,ldx", [(16, 256, 256), (1, 4096, 4096), (7, 128, 136), (65, 14336, 14336),
+                                     (1000, 1024, 1024)])
+def test_quantize_activations_bit_exact(gpu_lib, M, K, ldx):
+    X = synth.activations_fp16(M, ldx, seed=M)
+    if M > 3:
+        X[2] = 0
+        X[3] = np.float16(2e-6) * np.sign(X[3])   # s_x underflow / clamp regime
+    qx, sx, tx = gpu_lib.quantize_activations_per_token(to_dev(X), K)
+    qx_ref, sx_ref, tx_ref = oracle.quantize_activations(X, K)
+    assert np.array_equal(bits16(sx), sx_ref.view(np.uint16))
+    assert np.array_equal(qx.cpu().numpy(), qx_ref)
+    assert np.array_equal(tx.cpu().numpy(), tx_ref)
+
+
+def test_quantize_activations_all_fp16_magnitudes(gpu_lib):
+    """Every positive finite fp16 value as a row max (incl. subnormal-scale regimes)."""
+    a = np.arange(1, 0x7c00, dtype=np.uint16).view(np.float16)
+    X = np.zeros((a.size, 8), np.float16)
+    X[:, 0] = a
+    X[:, 1] = -a / 3
+    X[:, 2] = a / 7
+    qx, sx, tx = gpu_lib.quantize_activations_per_token(to_dev(X))
+    qx_ref, sx_ref, tx_ref = oracle.quantize_activations(X)
+    assert np.array_equal(bits16(sx), sx_ref.view(np.uint16))
+    assert np.array_equal(qx.cpu().numpy(), qx_ref)
+
+
+# ------------------------------------------------------------------ GEMM
+
+def _case(M, N, K, seed):
+    W = synth.weights_fp16(N, K, seed=seed)
+    X = synth.activations_fp16(M, K, seed=seed)
+    p_ref, s0_ref = oracle.quantize_weights(W)
+    qx_ref, sx_ref, tx_ref = oracle.quantize_activations(X)
+    return W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref
+
+
+GEMM_SHAPES = [(16, 256, 256), (1, 128, 128), (7, 256, 1024), (63, 1280, 256), (64, 128, 4096),
+               (65, 384, 512), (129, 256, 384), (256, 512, 256), (300, 1280, 1024)]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+@pytest.mark.parametrize("use_tx", [True, False])
+def test_gemm_i32_bit_exact(gpu_lib, M, N, K, use_tx):
+    W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=M * 7 + N + K)
+    packed = to_dev(p_ref)
+    acc = gpu_lib.w4a8_gemm_i32(to_dev(qx_ref), to_dev(tx_ref) if use_tx else None, packed, N)
+    acc_ref = oracle.acc_from_packed(qx_ref, p_ref, N, K)
+    a = acc.cpu().numpy()
+    assert np.array_equal(a, acc_ref), f"{(a != acc_ref).sum()} accumulators differ"
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_fp16_within_tolerance(gpu_lib, M, N, K):
+    W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=M + 3 * N + K)
+    Y = gpu_lib.w4a8_gemm(to_dev(qx_ref), to_dev(sx_ref), to_dev(tx_ref), to_dev(p_ref), to_dev(s0_ref), N)
+    y_ref = oracle.epilogue_f64(oracle.acc_from_packed(qx_ref, p_ref, N, K), sx_ref, s0_ref)
+    check_y(Y, y_ref)
+
+
+def test_full_path_config1_and_workspace_restored(gpu_lib):
+    """Config 1 end to end on device (quantize weights, quantize X, GEMM) and the split-K
+    workspace returns to all-zero after the call."""
+    M, N, K = 16, 256, 256
+    W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=0)
+    ws = gpu_lib.Workspace(dev())
+    packed, s0 = gpu_lib.quantize_weights(to_dev(W))
+    Y = gpu_lib.linear(to_dev(X), packed, s0, N, workspace=ws)
+    torch.cuda.synchronize()
+    check_y(Y, oracle.linear_rows(X, p_ref, s0_ref, N))
+    if ws.buf is not None:
+        assert int(ws.buf.count_nonzero()) == 0
+
+
+def test_gemm_matches_library_w8a8_on_dequantized_weights(gpu_lib):
+    """Library cross-check (W8A8 reduction, "as if it was W8A8"): the W4A8 accumulators equal
+    cuBLASLt's INT8 GEMM (torch._int_mm) on the level-2-dequantized INT8 weights q̂."""
+    M, N, K = 64, 1280, 1024
+    W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=11)
+    qu4, s, z = oracle.unpack(p_ref, N, K)
+    qhat = oracle.dequant_level2(qu4, s, z).astype(np.int8)
+    ref = torch._int_mm(to_dev(qx_ref), to_dev(qhat).t())   # [K][N] column-major view
+    acc = gpu_lib.w4a8_gemm_i32(to_dev(qx_ref), to_dev(tx_ref), to_dev(p_ref), N)
+    assert torch.equal(acc, ref)
+
+
+@pytest.mark.parametrize("name,N,K", [(n, N, K) for n, N, K, _ in synth.LLAMA3_8B])
+@pytest.mark.parametrize("M", [1, 64])
+def test_llama3_8b_full_size_sampled(gpu_lib, name, N, K, M):
+    """Full Llama-3-8B shapes at decode M in the launch configuration bench.py times: every output
+    of sampled rows against the oracle (INT32 exact on the sample, Y within tolerance)."""
+    W = synth.weights_fp16(N, K, seed=1)
+    X = synth.activations_fp16(M, K, seed=1)
+    p_ref, s0_ref = oracle.quantize_weights(W)
+    packed, s0 = gpu_lib.quantize_weights(to_dev(W))
+    assert np.array_equal(packed.cpu().numpy(), p_ref)           # full-size packing, bit-exact
+    assert np.array_equal(bits16(s0), s0_ref.view(np.uint16))
+    qx, sx, tx = gpu_lib.quantize_activations_per_token(to_dev(X))
+    Y = gpu_lib.w4a8_gemm(qx, sx, tx, packed, s0, N)
+    acc = gpu_lib.w4a8_gemm_i32(qx, tx, packed, N)
+    rows = sorted({0, M - 1, M // 2})
+    y_ref = oracle.linear_rows(X[rows], p_ref, s0_ref, N)
+    check_y(Y[rows], y_ref)
+    qx_ref, _, _ = oracle.quantize_activations(X[rows])
+    acc_ref = oracle.acc_from_packed(qx_ref, p_ref, N, K)
+    assert np.array_equal(acc[rows].cpu().numpy(), acc_ref)
+
+
+def test_linear_host_e2e(gpu_lib):
+    M, N, K = 64, 1280, 1024
+    W, X, p_ref, s0_ref, *_ = _case(M, N, K, seed=5)
+    Xh = torch.from_numpy(X).pin_memory()
+    Yh = torch.empty(M, N, dtype=torch.float16).pin_memory()
+    scratch = torch.zeros(gpu_lib.linear_host_scratch_bytes(M, N, K), dtype=torch.uint8, device=dev())
+    gpu_lib.linear_host(Xh, to_dev(p_ref), to_dev(s0_ref), N, Yh, scratch)
+    torch.cuda.synchronize()
+    check_y(Yh, oracle.linear_rows(X, p_ref, s0_ref, N))
