@@ -1,0 +1,556 @@
+"""bench.py — throughput of the QoQ W4A8 hot path on B200 (BASELINE.json metric:
+"W4A8 GEMM TOPS (frac of INT8 tensor peak) and HBM GB/s at decode M, 1-8 B200").
+
+One STEP = one decode pass of the whole hot path over all linear layers of a Llama-3-8B-shaped
+model (32 layers x {qkv, o, gate, up, down}, plus a8 when N > 1), in the
+paper's precision mapping (Fig. 7): per layer 4 per-token activation quantizations
+(before qkv, o, gate/up, down) and 5 W4A8 GEMMs. Weights are packed offline (row a1) before timing.
+The 32-layer packed weight stack (3.6 GB) is far larger than the 126 MB L2, so every step streams
+weights from HBM (no flush needed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--M 64] [--impl ours|reference]
+
+N > 1 (torchrun): Megatron tensor parallelism — qkv/gate/up column-sharded over N (no
+collective), o/down row-sharded over K at group boundaries with an NCCL all-reduce of the fp16
+partials; total work is fixed ("strong" scaling).
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "W4A8 GEMM HBM GB/s at decode M (Llama-3-8B linear layers, quantizer + GEMM per step)"
+UNIT = "GB/s"
+FALLBACK_HBM_GBS = 6650.0          # B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json is absent)
+INT8_DATASHEET_TOPS = 4500.0       # dense INT8 tensor peak, datasheet
+
+
+# ------------------------------------------------------------------ algorithmic work
+
+def gemm_bytes(M, N, K):
+    """What the method must move: u4 codes + s_u8/zs + s0 + q_x + s_x + t_x + Y."""
+    return N * K // 2 + 2 * N * (K // 128) + 2 * N + M * K + 2 * M + 4 * M + 2 * M * N
+
+
+def quant_bytes(M, K):
+    """Per-token quantizer: read X fp16, write q_x, s_x, t_x."""
+    return 2 * M * K + M * K + 2 * M + 4 * M
+
+
+def gemm_ops(M, N, K):
+    return 2 * M * N * K
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(config_key):
+    """dram bytes per GEMM launch from a committed `ncu --set full` capture, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config_key)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ model layout and TP sharding
+
+def layer_shapes(model, M, world, rank):
+    """Per-rank GEMM list of one layer: (name, N_r, K_r, kind, quant_group). Column-parallel layers
+    split N, row-parallel layers split K (both at 128 boundaries). quant_group names which
+    activation quantization feeds the GEMM (gate and up share one, as in Fig. 7)."""
+    shapes, _ = synth.MODELS[model]
+    out = []
+    for name, N, K, kind in shapes:
+        if kind == "col":
+            assert N % (128 * world) == 0
+            Nr, Kr = N // world, K
+        else:
+            assert K % (128 * world) == 0
+            Nr, Kr = N, K // world
+        qg = {"qkv": "attn_in", "o": "attn_out", "gate": "mlp_in", "up": "mlp_in", "down": "mlp_act"}[name]
+        out.append((name, Nr, Kr, kind, qg))
+    return out
+
+
+def step_work(model, M, layers, world):
+    """Whole-job algorithmic bytes / ops of one step (all ranks together)."""
+    b = ops = 0
+    for name, N, K, kind in synth.MODELS[model][0]:
+        b += gemm_bytes(M, N, K) * layers
+        ops += gemm_ops(M, N, K) * layers
+    shapes = {n: (N, K) for n, N, K, _ in synth.MODELS[model][0]}
+    for src in ("qkv", "o", "gate", "down"):
+        b += quant_bytes(M, shapes[src][1]) * layers
+    return b, ops
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index):
+        self.samples = []
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _reasons(self):
+        try:
+            return self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            return self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append((self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM), self._reasons()))
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        mhz = [s for s, _ in self.samples]
+        bits = 0
+        for _, r in self.samples:
+            bits |= r
+        return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": self.max_mhz,
+                "reasons": [n for b, n in self.REASONS.items() if bits & b], "samples": len(mhz)}
+
+
+# ------------------------------------------------------------------ reference arm / cpu baseline (the oracle)
+
+def oracle_sample(seconds_min=10.0, reps_max=200, M=64):
+    """The CPU oracle, as it stands, on a bounded sample of the workload: layer 0's o_proj
+    (4096x4096, g=128) at decode M, full work (O4 quantize -> O3^-1 unpack -> level-2 dequant ->
+    O5 INT32 GEMM -> O6 fp64 epilogue), repeated until >= seconds_min. Returns (GB/s, detail)."""
+    import oracle
+    N, K = 4096, 4096
+    W = synth.weights_fp16(N, K, seed=0)
+    X = synth.activations_fp16(M, K, seed=0)
+    packed, s0 = oracle.quantize_weights(W)
+    t0 = time.perf_counter()
+    reps = 0
+    while reps < reps_max:
+        oracle.linear_rows(X, packed, s0, N)
+        reps += 1
+        if time.perf_counter() - t0 >= seconds_min:
+            break
+    dt = time.perf_counter() - t0
+    b = (gemm_bytes(M, N, K) + quant_bytes(M, K)) * reps
+    return b / dt / 1e9, {"reps": reps, "seconds": dt, "threads": oracle.num_threads(),
+                           "sample": f"layer-0 o_proj {N}x{K} g128 at M={M}, quantize+GEMM+epilogue, x{reps}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    M = args.M
+    N, K = 4096, 4096
+    W = synth.weights_fp16(N, K, seed=0)
+    X = synth.activations_fp16(M, K, seed=0)
+    packed, s0 = oracle.quantize_weights(W)
+    for _ in range(args.warmup):
+        oracle.linear_rows(X, packed, s0, N)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.linear_rows(X, packed, s0, N)
+    dt = time.perf_counter() - t0
+    b = (gemm_bytes(M, N, K) + quant_bytes(M, K)) * args.steps
+    v = b / dt / 1e9
+    sample = f"each step: layer-0 o_proj {N}x{K} g128 at M={M} (quantize + W4A8 GEMM + epilogue) on the CPU oracle"
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": config_dict(args, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def config_dict(args, world):
+    layers = args.layers or synth.MODELS[args.model][1]
+    return {"workload": f"{args.model} decode linear stack: {layers} layers x (qkv, o, gate, up, down), "
+                        f"M={args.M} tokens, W4A8 g128, per-token INT8 activations",
+            "model_shapes": args.model, "M": args.M, "layers": layers, "group": 128,
+            "parallelism": f"tp{world}" if world > 1 else "single",
+            "l2": "weights stream from HBM: packed stack >> 126 MB L2 (no flush needed)"}
+
+
+# ------------------------------------------------------------------ our arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--M", type=int, default=64)
+    ap.add_argument("--model", default="llama3-8b", choices=list(synth.MODELS))
+    ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--prefill-M", type=int, default=4096)
+    ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--detail", action="store_true", help="per-projection GEMM breakdown and M sweep")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_04532_b200 as qoq
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    qoq.load()
+    M = args.M
+    layers = args.layers or synth.MODELS[args.model][1]
+    shapes = layer_shapes(args.model, M, world, rank)
+    stream = torch.cuda.Stream(dev)
+
+    # ---- offline: pack every layer's weights on device (row a1), distinct per layer
+    packed = []   # [layer][i] -> (packed, s0)
+    gen = torch.Generator(device=dev)
+    with torch.cuda.stream(stream):
+        for l in range(layers):
+            row = []
+            for i, (name, N, K, kind, qg) in enumerate(shapes):
+                gen.manual_seed(1000 * l + 17 * i + rank)
+                W = synth.device_weights_fp16(N, K, gen, dev)
+                row.append(qoq.quantize_weights(W, stream=stream))
+                del W
+            packed.append(row)
+    stream.synchronize()
+
+    # ---- activations (L2-resident, as when produced by the preceding kernel in a real decode)
+    gen.manual_seed(7)
+    Kin = {}
+    for name, N, K, kind, qg in shapes:
+        Kin[qg] = K
+    X = {qg: synth.device_activations_fp16(M, K, gen, dev) for qg, K in Kin.items()}
+    quant_out = {qg: (torch.empty(M, K, dtype=torch.int8, device=dev), torch.empty(M, dtype=torch.float16, device=dev),
+                      torch.empty(M, dtype=torch.int32, device=dev)) for qg, K in Kin.items()}
+    Ybuf = {name: torch.empty(M, N, dtype=torch.float16, device=dev) for name, N, K, kind, qg in shapes}
+    ws = qoq.Workspace(dev)
+    ws.get(max(qoq.gemm_workspace_bytes(M, N, K) for _, N, K, _, _ in shapes))
+
+    def run_step(gemm_only=False):
+        n_launch = 0
+        for l in range(layers):
+            done = set()
+            for i, (name, N, K, kind, qg) in enumerate(shapes):
+                if not gemm_only and qg not in done:
+                    qoq.quantize_activations_per_token(X[qg], out=quant_out[qg], stream=stream)
+                    done.add(qg)
+                    n_launch += 1
+                qx, sx, tx = quant_out[qg]
+                p, s0 = packed[l][i]
+                qoq.w4a8_gemm(qx, sx, tx, p, s0, N, out=Ybuf[name], workspace=ws, stream=stream)
+                n_launch += 1
+                if kind == "row" and world > 1 and not gemm_only:
+                    dist.all_reduce(Ybuf[name])
+        return n_launch
+
+    # ---- capture one step as a CUDA graph (launch gaps removed; PDL edges kept)
+    with torch.cuda.stream(stream):
+        run_step()
+        run_step(gemm_only=True)
+    stream.synchronize()
+    g_step = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_step, stream=stream):
+        launches_per_step = run_step()
+    g_gemm = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_gemm, stream=stream):
+        gemm_launches = run_step(gemm_only=True)
+
+    def timed(graph, steps, warmup):
+        for _ in range(warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    with torch.cuda.stream(stream):
+        sampler = ClockSampler(local)
+        for _ in range(args.warmup):
+            g_step.replay()
+        with sampler:
+            ms_total = timed(g_step, args.steps, 0)
+        ms_gemm = timed(g_gemm, max(10, args.steps // 2), 2)
+
+    ms_step = ms_total / args.steps
+    step_bytes, step_ops = step_work(args.model, M, layers, world)
+    value = step_bytes / (ms_step * 1e-3) / 1e9
+
+    # dominant kernel: the W4A8 GEMM (per-rank launches in the gemm-only graph)
+    rank_gemm_bytes = sum(gemm_bytes(M, N, K) for _, N, K, _, _ in shapes) * layers
+    per_launch_ms = ms_gemm / max(10, args.steps // 2) / gemm_launches
+    per_launch_bytes = rank_gemm_bytes / gemm_launches
+    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    peak, peak_src = load_peaks()
+    traffic = load_traffic(f"{args.model}-M{M}")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "w4a8_gemm_kernel",
+                "algorithmic_bytes_per_launch": per_launch_bytes, "avg_launch_us": per_launch_ms * 1e3,
+                "peak_source": peak_src}
+    tops = step_ops / (ms_step * 1e-3) / 1e12
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic (seeded N(0,1/K) fp16 weights packed on device; N(0,1) fp16 activations "
+                    "with 0.1% x20 outlier channels)",
+            "config": config_dict(args, world), "gpu_launches": launches_per_step * args.steps,
+            "clocks": sampler.summary(), "roofline": roofline,
+            "decode_tops": tops, "decode_frac_int8_datasheet": tops / INT8_DATASHEET_TOPS}
+
+    # ---- e2e through the C ABI with host buffers (H2D + quantize + GEMM + D2H per GEMM)
+    if not args.no_e2e:
+        line["e2e"] = e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes)
+
+    if not args.no_prefill:
+        line["prefill"] = prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream)
+
+    if args.detail:
+        line["detail"] = detail_measure(qoq, torch, args, shapes, packed, layers, dev, stream, X)
+
+    if rank == 0 and not args.no_cpu_baseline:
+        v, d = oracle_sample()
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": d["threads"], "kind": "oracle",
+                                "sample": d["sample"]}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+    return 0
+
+
+def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes):
+    M = args.M
+    gen = torch.Generator().manual_seed(3)
+    Xh = {}
+    Yh = {}
+    for name, N, K, kind, qg in shapes:
+        Xh[name] = (torch.randn(M, K, generator=gen) * 1.0).half().pin_memory()
+        Yh[name] = torch.empty(M, N, dtype=torch.float16).pin_memory()
+    scratch = torch.zeros(max(qoq.linear_host_scratch_bytes(M, N, K) for _, N, K, _, _ in shapes),
+                          dtype=torch.uint8, device=dev)
+    h2d = sum(M * K * 2 for _, N, K, _, _ in shapes) * layers
+    d2h = sum(M * N * 2 for _, N, K, _, _ in shapes) * layers
+    red = {name: torch.empty(M, N, dtype=torch.float16, device=dev)
+           for name, N, K, kind, qg in shapes if kind == "row"}
+
+    def one_step():
+        for l in range(layers):
+            for i, (name, N, K, kind, qg) in enumerate(shapes):
+                p, s0 = packed[l][i]
+                qoq.linear_host(Xh[name], p, s0, N, Yh[name], scratch, stream=stream)
+                if kind == "row" and world > 1:
+                    with torch.cuda.stream(stream):
+                        red[name].copy_(Yh[name], non_blocking=True)
+                        dist.all_reduce(red[name])
+                        Yh[name].copy_(red[name], non_blocking=True)
+
+    steps = max(3, args.steps // 10)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            one_step()
+        stream.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            one_step()
+        e1.record(stream)
+        stream.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        h2d_rank, d2h_rank = h2d, d2h
+    else:
+        h2d_rank, d2h_rank = h2d, d2h
+    return {"value": step_bytes / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d_rank * world,
+            "d2h_bytes_per_step": d2h_rank * world, "ms_per_step": ms, "steps": steps,
+            "api": "qoq_linear_host (C ABI, pinned host X/Y) per GEMM"}
+
+
+def prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream):
+    """Tensor-bound regime (BASELINE configs[2]): GEMM-only TOPS at M = prefill_M over the first
+    4 layers' weights (rotating, > L2), and the INT8 ceiling measured with cuBLASLt in the same run."""
+    M = args.prefill_M
+    L = min(4, layers)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(11)
+    Ks = sorted({K for _, N, K, _, _ in shapes})
+    q = {}
+    for K in Ks:
+        Xp = synth.device_activations_fp16(M, K, gen, dev)
+        q[K] = qoq.quantize_activations_per_token(Xp, stream=stream)
+    Y = {name: torch.empty(M, N, dtype=torch.float16, device=dev) for name, N, K, kind, qg in shapes}
+    ws = qoq.Workspace(dev)
+
+    def run():
+        for l in range(L):
+            for i, (name, N, K, kind, qg) in enumerate(shapes):
+                qx, sx, tx = q[K]
+                p, s0 = packed[l][i]
+                qoq.w4a8_gemm(qx, sx, tx, p, s0, N, out=Y[name], workspace=ws, stream=stream)
+
+    with torch.cuda.stream(stream):
+        run()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            run()
+        for _ in range(3):
+            g.replay()
+        stream.synchronize()
+        reps = 5
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+        stream.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ops = sum(gemm_ops(M, N, K) for _, N, K, _, _ in shapes) * L
+    tops = ops / (ms * 1e-3) / 1e12
+    ceil = int8_ceiling(torch, dev)
+    return {"M": M, "layers": L, "tops": tops, "ms": ms,
+            "frac_int8_datasheet": tops / INT8_DATASHEET_TOPS,
+            "int8_ceiling_tops": ceil, "frac_int8_measured_ceiling": tops / ceil if ceil else None,
+            "ceiling_how": "torch._int_mm (cuBLASLt IMMA) 8192^3 best of 10, same run"}
+
+
+def int8_ceiling(torch, dev):
+    try:
+        a = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device=dev)
+        b = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device=dev).t()
+        torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(10):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
+def detail_measure(qoq, torch, args, shapes, packed, layers, dev, stream, X):
+    out = {}
+    M = args.M
+    for i, (name, N, K, kind, qg) in enumerate(shapes):
+        qx, sx, tx = qoq.quantize_activations_per_token(X[qg], stream=stream)
+        Y = torch.empty(M, N, dtype=torch.float16, device=dev)
+        ws = qoq.Workspace(dev)
+
+        def run():
+            for l in range(layers):
+                p, s0 = packed[l][i]
+                qoq.w4a8_gemm(qx, sx, tx, p, s0, N, out=Y, workspace=ws, stream=stream)
+
+        with torch.cuda.stream(stream):
+            run()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                run()
+            for _ in range(3):
+                g.replay()
+            stream.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(10):
+                g.replay()
+            e1.record(stream)
+            stream.synchronize()
+        us = e0.elapsed_time(e1) / 10 / layers * 1e3
+        out[name] = {"N": N, "K": K, "us": us, "GBps": gemm_bytes(M, N, K) / (us * 1e-6) / 1e9}
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -88,7 +88,7 @@ size_t qoq_gemm_workspace_bytes(int M, int N, int K);
  * with q_u4 expanded to INT8 in registers, contracted on tcgen05 INT8 tensor
  * cores with INT32 accumulation in tensor memory, scaled in the epilogue.
  *   qx [M][K] int8, sx_fp16 [M], tx [M] int32 or NULL (if given, must equal Σ_k qx[m][k]).
- *   packed / s0_fp16 from qoq_quantize_weights.  Y_fp16 [M][ldy], ldy >= N.
+ *   packed / s0_fp16 from qoq_quantize_weights.  Y_fp16 [M][ldy], ldy >= N, ldy % 4 == 0.
  * Requires group == 128, N % 128 == 0, K % 128 == 0, K <= 65536. M == 0 is a no-op. */
 int qoq_w4a8_gemm(const int8_t* qx, const void* sx_fp16, const int32_t* tx,
                   const void* packed, const void* s0_fp16,
@@ -97,7 +97,7 @@ int qoq_w4a8_gemm(const int8_t* qx, const void* sx_fp16, const int32_t* tx,
                   void* workspace, size_t workspace_bytes, void* stream);
 
 /* Parity/debug entry: the same main loop; the epilogue writes the exact INT32 accumulators
- * acc[m][n] = Σ_k qx[m][k] * q̂[n][k] (bias-corrected) into acc [M][ldacc] instead of Y. */
+ * acc[m][n] = Σ_k qx[m][k] * q̂[n][k] (bias-corrected) into acc [M][ldacc] (ldacc % 4 == 0). */
 int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed,
                       int M, int N, int K, int group,
                       int32_t* acc, int ldacc,

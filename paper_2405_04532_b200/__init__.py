@@ -18,7 +18,9 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqoq_b200.so")
+# QOQ_LIB_VARIANT selects a debug/ablation build (tools only); production uses libqoq_b200.so
+LIB_PATH = os.path.join(_HERE, "libqoq_b200.so" if not os.environ.get("QOQ_LIB_VARIANT")
+                        else f"libqoq_b200_{os.environ['QOQ_LIB_VARIANT']}.so")
 GROUP = 128
 TILE_BYTES = 8448
 ABI_VERSION = 1

@@ -8,6 +8,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqoq_b200.so")
+
+
+def lib_path(variant: str = "") -> str:
+    return LIB if not variant else os.path.join(HERE, f"libqoq_b200_{variant}.so")
 SOURCES = ["qoq_api.cu", "quantize.cu", "w4a8_gemm.cu"]
 HEADERS = ["qoq_internal.h", "sm100_ptx.cuh", os.path.join("..", "..", "include", "qoq_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -23,26 +27,33 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None, variant: str = "") -> str:
+    """variant != "": a debug/ablation build (e.g. extra=["-DQOQ_ABLATE=1"]) into libqoq_b200_<variant>.so."""
+    out = lib_path(variant)
+    if not force and not variant and not _stale():
         return LIB
     objs = []
     for s in SOURCES:
-        o = os.path.join(CSRC, s.replace(".cu", ".o"))
+        o = os.path.join(CSRC, s.replace(".cu", f"{variant}.o"))
         cmd = [NVCC, *FLAGS, *(extra or []), "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(o)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
                            "-o", tmp, *objs, "-lcuda" if False else "-ldl"])
-    os.replace(tmp, LIB)
+    os.replace(tmp, out)
     for o in objs:
         os.remove(o)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True,
-                extra=["-Xptxas", "-v"] if "--ptxas" in sys.argv else None))
+    extra = ["-Xptxas", "-v"] if "--ptxas" in sys.argv else []
+    variant = ""
+    for a in sys.argv[1:]:
+        if a.startswith("--ablate="):
+            variant = "ablate" + a.split("=")[1]
+            extra.append("-DQOQ_ABLATE=" + a.split("=")[1])
+    print(build(force="--force" in sys.argv or bool(variant), verbose=True, extra=extra, variant=variant))

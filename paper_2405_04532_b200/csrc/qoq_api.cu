@@ -41,17 +41,19 @@ int num_sms_or_default() {
 
 int run_gemm(const int8_t* qx, const void* sx, const int32_t* tx, const void* packed, const void* s0,
              int M, int N, int K, int group, void* out, int ldo, bool out_i32,
-             void* ws, size_t ws_bytes, cudaStream_t st) {
+             void* ws, size_t ws_bytes, cudaStream_t st, void* trace = nullptr) {
     int rc = gemm_shape_status(M, N, K, group);
     if (rc) return rc;
     if (M == 0) return QOQ_OK;
     if (!qx || !packed || !out || (!out_i32 && (!sx || !s0))) return QOQ_ERR_INVALID_ARG;
     if (!aligned16(qx) || !aligned16(packed) || ldo < N) return QOQ_ERR_INVALID_ARG;
+    // vectorized epilogue: 4 consecutive outputs per store, 8-byte aligned s0 loads
+    if (ldo % 4 != 0 || !aligned16(out) || (!out_i32 && !aligned16(s0))) return QOQ_ERR_INVALID_ARG;
     int sms = 0;
     if ((rc = check_arch(&sms))) return rc;
     GemmPlan p = plan_gemm(M, N, K, sms);
     if (p.ws_bytes > 0 && (!ws || ws_bytes < p.ws_bytes || !aligned16(ws))) return QOQ_ERR_WORKSPACE;
-    GemmArgs a{qx, sx, tx, packed, s0, out, ldo, out_i32, M, N, K, p.ws_bytes ? ws : nullptr};
+    GemmArgs a{qx, sx, tx, packed, s0, out, ldo, out_i32, M, N, K, p.ws_bytes ? ws : nullptr, trace};
     return launch_w4a8_gemm(a, p, st, /*pdl=*/true) == cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
 }
 
@@ -123,6 +125,15 @@ int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed, i
     if (ldacc < N) return QOQ_ERR_INVALID_ARG;
     return run_gemm(qx, nullptr, tx, packed, nullptr, M, N, K, group, acc, ldacc, true, ws, ws_bytes,
                     static_cast<cudaStream_t>(stream));
+}
+
+// Debug (not in the public header): the fp16 GEMM with a per-CTA %globaltimer trace
+// (16 x u64 per CTA, grid <= #SMs) for pipeline timeline analysis (tools/trace_gemm.py).
+int qoq_debug_w4a8_gemm_trace(const int8_t* qx, const void* sx, const int32_t* tx, const void* packed,
+                              const void* s0, int M, int N, int K, void* Y, void* ws, size_t ws_bytes,
+                              void* trace, void* stream) {
+    return run_gemm(qx, sx, tx, packed, s0, M, N, K, 128, Y, N, false, ws, ws_bytes,
+                    static_cast<cudaStream_t>(stream), trace);
 }
 
 // scratch layout: [X fp16 M*K][qx M*K][sx 2M][tx 4M][Y fp16 M*N][gemm workspace], each 256-B aligned

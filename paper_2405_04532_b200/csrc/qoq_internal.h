@@ -16,10 +16,12 @@ constexpr int kTileBytes = 8448;     // 8192 B of u4 codes + 128 B s_u8 + 128 B 
 struct GemmPlan {
     int BN;          // token tile = MMA N (16, 32, 64, 128 or 256)
     int MT, NT, KT;  // token tiles, 128-row weight tiles, 128-deep K tiles
+    int KS;          // pipeline steps per output tile (2 k-tiles each, last may hold 1)
     int T;           // output tiles = MT * NT
-    long long I;     // k-iterations = T * KT
+    long long I;     // steps = T * KS
     int G;           // CTAs (persistent, <= #SMs)
-    int mode;        // 0: whole tiles round-robin; 1: contiguous k-iteration ranges (split-K)
+    int mode;        // 0: whole tiles round-robin; 1: stream-K (global workspace); 2: S-CTA cluster split-K
+    int S;           // mode 2: CTAs (cluster size) per output tile
     size_t ws_bytes; // INT32 partials + per-tile counters (mode 1), else 0
 };
 
@@ -36,6 +38,7 @@ struct GemmArgs {
     bool out_i32;
     int M, N, K;
     void* ws;
+    void* trace = nullptr;   // debug timeline buffer (16 u64 per CTA) or nullptr
 };
 
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl);

@@ -26,28 +26,60 @@
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "qoq_internal.h"
 #include "sm100_ptx.cuh"
 
+// Timing ablations (never in production builds; results are garbage when set):
+//   2: no activation TMA (xfull arrives without data)   4: no weight bulk copies (wfull arrives)
+//   8: dequant skips the ALU expansion
+#ifndef QOQ_ABLATE
+#define QOQ_ABLATE 0
+#endif
+
 namespace qoq {
 
-constexpr int kThreads = 384;       // warps: 0 producer, 1 MMA + TMEM owner, 2-3 idle, 4-7 dequant, 8-11 epilogue
-constexpr int kAStages = 4;         // TMEM buffers for expanded weight tiles (32 columns each)
+constexpr int kThreads = 448;       // + 64 below: warps 0 weight producer, 1 MMA issuer 0 + TMEM owner,
+                                    // 2-9 dequant, 10-13 epilogue, 14 MMA issuer 1, 15 activation producer
+constexpr int kEpiThread0 = 320;    // first epilogue thread (warps 10-13)
 
+// One pipeline STEP = up to two consecutive 128-deep k-tiles of one output tile: the handoff
+// (dequant -> MMA, MMA -> producer) is amortized over 8 MMAs, and two MMA-issuing warps take
+// alternate steps of a segment into separate accumulators (summed in the epilogue). Measured on
+// B200 (tools/mma_bench2.cu): one issuer, one tile per handoff ~520 cycles per 128x128 tile; two
+// issuers, two tiles per handoff ~193 cycles (MMA floor at N <= 64: 4 x 45 cycles).
 template <int BN>
 struct Cfg {
-    static constexpr int kActBytes = BN * 128;
-    static constexpr int kStageBytes = ((kActBytes + kTileBytes + 1023) / 1024) * 1024;
-    static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
-    static constexpr int kStages = kStagesRaw > 16 ? 16 : kStagesRaw;
-    static constexpr int kAccStages = BN <= 128 ? 2 : 1;
-    static constexpr int kColsUsed = kAStages * 32 + kAccStages * BN;
+    static constexpr int kIssuers = BN <= 128 ? 2 : 1;
+    static constexpr int kActBytes = BN * 128;                        // one k-tile of activations
+    static constexpr int kXStageBytes = 2 * kActBytes;                // activations of one step (1024-aligned)
+    static constexpr int kChunk = BN < 32 ? BN : 32;                  // TMEM columns per epilogue tcgen05.ld
+    static constexpr int kStgBytes = kChunk * 128 * 4;                // one INT32 staging buffer [kChunk][128]
+    static constexpr int kEpiBytes = 2 * kStgBytes + BN * 8;          // 2 staging buffers + per-token s_x, 128 t_x
+    static constexpr int kAccStages = (2 * kIssuers * BN + 4 * 64 <= 512) ? 2 : 1;
+    static constexpr int kAccCols = kAccStages * kIssuers * BN;
+    // Three independent rings: W (packed weights, HBM-latency bound, SMEM), X (activation k-tiles,
+    // L2-latency bound, SMEM) and A (expanded weights, 64 TMEM columns per step). (Loading weights
+    // straight from L2 into registers after a bulk L2 prefetch was measured slower on B200: the
+    // register loads stall at HBM latency with too few bytes in flight per SM.)
+    static constexpr int kARaw = (512 - kAccCols) / 64;
+    static constexpr int kAStages = kARaw > 6 ? 6 : kARaw;
+    static constexpr int kXStages = BN <= 32 ? 8 : BN == 64 ? 6 : BN == 128 ? 3 : 2;
+    static constexpr int kWStageBytes = ((2 * kTileBytes + 1023) / 1024) * 1024;   // packed weights of one step
+    static constexpr int kWRaw = (212 * 1024 - kEpiBytes - kXStages * kXStageBytes) / kWStageBytes;
+    static constexpr int kWStages = kWRaw > 8 ? 8 : kWRaw;
+    static constexpr int kColsUsed = kAStages * 64 + kAccCols;
     static constexpr int kTmemCols = kColsUsed <= 32 ? 32 : kColsUsed <= 64 ? 64 : kColsUsed <= 128 ? 128
                                    : kColsUsed <= 256 ? 256 : 512;
-    static constexpr int kBarBytes = 8 * (2 * kStages + 2 * kAStages + 2 * kAccStages) + 16;
-    static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes;
-    static constexpr int kChunk = BN < 32 ? BN : 32;   // TMEM columns per epilogue tcgen05.ld
+    static constexpr int kXOff = 0;
+    static constexpr int kWOff = kXStages * kXStageBytes;
+    static constexpr int kEpiOff = kWOff + kWStages * kWStageBytes;
+    static constexpr int kBarOff = kEpiOff + kEpiBytes;
+    static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kXStages + 2 * kAStages + 2 * kAccStages + 1) + 16;
+    static constexpr int kSmemBytes = 1024 + kBarOff + kBarBytes;
+    static constexpr int kFinU = BN / 4 < 8 ? BN / 4 : 8;             // independent 16-B loads per finalize batch
+    static_assert(kXStages >= 2 && kWStages >= 2 && kAStages >= 2, "pipeline too shallow");
     static_assert(kColsUsed <= 512, "TMEM overflow");
     static_assert(kSmemBytes <= 227 * 1024, "SMEM overflow");
 };
@@ -61,82 +93,138 @@ struct KParams {
     int ldo;
     int32_t* ws;
     int* counters;
-    int M, MT, KT, T, G, mode;
-    long long I;
+    int M, MT, KT, KS, T, G, mode, S;   // mode 2: S-CTA clusters split one tile's K range
+    long long I;                 // total steps = T * KS
+    unsigned long long* trace;   // debug: per-CTA %globaltimer stamps (nullptr in production)
 };
 
-// Iterates the (tile, k0, k1) segments one CTA owns. Every role runs an identical copy.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define QOQ_TRACE(p, ev) \
+    do { if ((p).trace) (p).trace[blockIdx.x * 16 + (ev)] = gtimer(); } while (0)
+// per-iteration stamps of CTA 0 use the SM cycle counter (clock64), cycle-accurate within the SM
+#define QOQ_TRACE_IT(p, it, ev) \
+    do { if ((p).trace && blockIdx.x == 0 && (it) < 64) (p).trace[148 * 16 + (it) * 8 + (ev)] = clock64(); } while (0)
+
+// Iterates the (tile, s0, s1) segments (ranges of steps of one output tile) a CTA owns.
+// Every role runs an identical copy.
 struct SegIter {
     long long cur, end;
-    int b, G, KT, T, mode;
-    __device__ SegIter(const KParams& p) : b(blockIdx.x), G(p.G), KT(p.KT), T(p.T), mode(p.mode) {
+    int b, G, KS, T, mode;
+    __device__ SegIter(const KParams& p) : b(blockIdx.x), G(p.G), KS(p.KS), T(p.T), mode(p.mode) {
         if (mode == 0) {
             cur = 0;
             end = 0;
+        } else if (mode == 2) {   // one segment: tile b / S, steps [c KS / S, (c+1) KS / S), c = rank in cluster
+            const int c = b % p.S, tile = b / p.S;
+            cur = (long long)tile * KS + (long long)c * KS / p.S;
+            end = (long long)tile * KS + (long long)(c + 1) * KS / p.S;
         } else {
             cur = (long long)b * p.I / p.G;
             end = (long long)(b + 1) * p.I / p.G;
         }
     }
-    __device__ bool next(int& tile, int& k0, int& k1) {
+    __device__ bool next(int& tile, int& s0, int& s1) {
         if (mode == 0) {
             const long long t = b + cur * G;
             if (t >= T) return false;
             tile = (int)t;
-            k0 = 0;
-            k1 = KT;
+            s0 = 0;
+            s1 = KS;
             ++cur;
             return true;
         }
         if (cur >= end) return false;
-        tile = (int)(cur / KT);
-        k0 = (int)(cur % KT);
+        tile = (int)(cur / KS);
+        s0 = (int)(cur % KS);
         const long long rem = end - cur;
-        k1 = (int)((long long)k0 + rem < KT ? k0 + rem : KT);
-        cur += k1 - k0;
+        s1 = (int)((long long)s0 + rem < KS ? s0 + rem : KS);
+        cur += s1 - s0;
         return true;
     }
 };
 
-template <int BN, bool OUT_I32>
-__device__ __forceinline__ void store_out(const KParams& p, int m, int n, int32_t a, float s0f) {
+// Four consecutive outputs Y[m][n..n+3] (or acc) from four INT32 accumulators.
+template <bool OUT_I32>
+__device__ __forceinline__ void write_out4(const KParams& p, int m, int n, int4 a, int bias, float sxf,
+                                           const float (&s0v)[4]) {
+    a.x -= bias; a.y -= bias; a.z -= bias; a.w -= bias;
     if constexpr (OUT_I32) {
-        static_cast<int32_t*>(p.out)[(size_t)m * p.ldo + n] = a;
+        *reinterpret_cast<int4*>(static_cast<int32_t*>(p.out) + (size_t)m * p.ldo + n) = a;
     } else {
-        const float sxf = __half2float(__ldg(p.sx + m));
-        static_cast<__half*>(p.out)[(size_t)m * p.ldo + n] = __float2half_rn((float)a * (sxf * s0f));
+        __half2 lo = __halves2half2(__float2half_rn((float)a.x * (sxf * s0v[0])),
+                                    __float2half_rn((float)a.y * (sxf * s0v[1])));
+        __half2 hi = __halves2half2(__float2half_rn((float)a.z * (sxf * s0v[2])),
+                                    __float2half_rn((float)a.w * (sxf * s0v[3])));
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&lo);
+        u.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(static_cast<__half*>(p.out) + (size_t)m * p.ldo + n) = u;
     }
 }
 
+template <int BN>
+__device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<BN>::kChunk]) {
+    if constexpr (Cfg<BN>::kChunk == 32) tmem_ld_32x32b_x32(taddr, v);
+    else tmem_ld_32x32b_x16(taddr, v);
+}
+
 template <int BN, bool OUT_I32>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads + 64, 1)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
-    uint64_t* empty = full + C::kStages;
-    uint64_t* afull = empty + C::kStages;
-    uint64_t* aempty = afull + kAStages;
-    uint64_t* accfull = aempty + kAStages;
+    // 1024-B aligned base derived by pointer arithmetic on the __shared__ array, so the compiler keeps
+    // the shared address space (LDS/STS, not generic LD/ST) for everything carved from it
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    int32_t* stg = reinterpret_cast<int32_t*>(smem + C::kEpiOff);   // [2][kChunk][128]
+    float* sxs = reinterpret_cast<float*>(smem + C::kEpiOff + 2 * C::kStgBytes);
+    int* txs = reinterpret_cast<int*>(sxs + BN);
+    uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + C::kBarOff);   // weights of W stage landed
+    uint64_t* wfree = wfull + C::kWStages;    // weights of W stage copied to registers (4 warps)
+    uint64_t* xfull = wfree + C::kWStages;    // activations of X slot landed (TMA)
+    uint64_t* xempty = xfull + C::kXStages;   // MMAs reading X slot complete (commit)
+    uint64_t* afull = xempty + C::kXStages;   // expanded step in TMEM buffer a (4 dequant warps)
+    uint64_t* aempty = afull + C::kAStages;   // MMAs reading TMEM buffer a complete (commit)
+    uint64_t* accfull = aempty + C::kAStages; // both issuers committed the accumulator stage
     uint64_t* accempty = accfull + C::kAccStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::kAccStages);
+    uint64_t* red_full = accempty + C::kAccStages;   // mode 2 leader: all S partials reduced into stg
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_full + 1);
     volatile int* fin_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) QOQ_TRACE(p, 0);
+    const bool clustered = (p.mode == 2);
+    const bool leader = clustered && cluster_ctarank() == 0;
+    if (leader) {   // zero the reduction target (the epilogue staging area) for the bulk reduce-adds
+        for (int i = threadIdx.x; i < BN * 128; i += blockDim.x) stg[i] = 0;
+        fence_proxy_async_smem();
+    }
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < C::kStages; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 4 + 1);   // 4 dequant warps + 1 MMA commit
+        if (leader) {
+            mbar_init(red_full, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(red_full, (uint32_t)(p.S * BN * 128 * 4));
         }
-        for (int i = 0; i < kAStages; ++i) {
+        for (int i = 0; i < C::kWStages; ++i) {
+            mbar_init(&wfull[i], 1);
+            mbar_init(&wfree[i], 4);
+        }
+        for (int i = 0; i < C::kXStages; ++i) {
+            mbar_init(&xfull[i], 1);
+            mbar_init(&xempty[i], 1);
+        }
+        for (int i = 0; i < C::kAStages; ++i) {
             mbar_init(&afull[i], 4);
             mbar_init(&aempty[i], 1);
         }
         for (int i = 0; i < C::kAccStages; ++i) {
-            mbar_init(&accfull[i], 1);
+            mbar_init(&accfull[i], C::kIssuers);
             mbar_init(&accempty[i], 4);
         }
         fence_mbar_init();
@@ -148,173 +236,348 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (clustered) cluster_sync_all();   // leader's zeroed target + armed red_full visible cluster-wide
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) QOQ_TRACE(p, 1);
 
-    pdl_wait();   // inputs produced by the previous kernel in the stream are visible from here on
-
+    // PDL: weights and scales are static, so the weight producer streams them without waiting for the
+    // previous kernel; everything that reads what the previous kernel wrote (q_x via TMA, s_x, t_x,
+    // the split-K workspace) sits behind griddepcontrol.wait.
     if (warp == 0) {
-        // ===================== producer: TMA activations + bulk-copy packed weights
+        // ===================== weight producer: per step, 1-2 packed 8448-B tiles via cp.async.bulk.
+        // Weights are static, so it runs ahead of griddepcontrol.wait (overlaps the previous kernel).
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();   // each weight byte is read once
             SegIter si(p);
-            int tile, k0, k1, stage = 0;
-            uint32_t phase = 0;
-            while (si.next(tile, k0, k1)) {
-                const int nt = tile / p.MT, mt = tile % p.MT;
-                for (int kt = k0; kt < k1; ++kt) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* st = smem + stage * C::kStageBytes;
-                    mbar_arrive_expect_tx(&full[stage], C::kActBytes + kTileBytes);
-                    tma_load_2d(st, &tmap_x, kt * 128, mt * BN, &full[stage]);
-                    bulk_g2s(st + C::kActBytes, p.packed + ((size_t)nt * p.KT + kt) * kTileBytes, kTileBytes,
-                             &full[stage], pol);
-                    if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+            int tile, s0, s1, ws = 0;
+            uint32_t wph = 0;
+            while (si.next(tile, s0, s1)) {
+                const int nt = tile / p.MT;
+                for (int sg = s0; sg < s1; ++sg) {
+                    const int kt0 = 2 * sg, nk = (kt0 + 1 < p.KT) ? 2 : 1;
+                    mbar_wait(&wfree[ws], wph ^ 1);
+                    uint8_t* dst = smem + C::kWOff + ws * C::kWStageBytes;
+                    if (QOQ_ABLATE & 4) {
+                        mbar_arrive(&wfull[ws]);
+                    } else {
+                        mbar_arrive_expect_tx(&wfull[ws], nk * kTileBytes);
+                        bulk_g2s(dst, p.packed + ((size_t)nt * p.KT + kt0) * kTileBytes, nk * kTileBytes, &wfull[ws],
+                                 pol);   // the step's 1-2 tiles are contiguous in the tile stream
+                    }
+                    if (++ws == C::kWStages) { ws = 0; wph ^= 1; }
                 }
             }
         }
-    } else if (warp == 1) {
-        // ===================== MMA issuer (single thread)
+    } else if (warp == 15) {
+        // ===================== activation producer: TMA 2-D (SWIZZLE_128B) k-tiles of q_x
         if (lane == 0) {
+            pdl_wait();
+            QOQ_TRACE(p, 2);
+            SegIter si(p);
+            int tile, s0, s1, xs = 0, it = 0;
+            uint32_t xph = 0;
+            while (si.next(tile, s0, s1)) {
+                const int mt = tile % p.MT;
+                for (int sg = s0; sg < s1; ++sg, ++it) {
+                    const int kt0 = 2 * sg, nk = (kt0 + 1 < p.KT) ? 2 : 1;
+                    mbar_wait(&xempty[xs], xph ^ 1);         // previous step of this slot consumed by the MMAs
+                    QOQ_TRACE_IT(p, it, 7);
+                    uint8_t* dst = smem + C::kXOff + xs * C::kXStageBytes;
+                    if ((QOQ_ABLATE & 2) && it >= C::kXStages) {
+                        mbar_arrive(&xfull[xs]);
+                    } else {
+                        mbar_arrive_expect_tx(&xfull[xs], nk * C::kActBytes);
+                        for (int t = 0; t < nk; ++t)
+                            tma_load_2d(dst + t * C::kActBytes, &tmap_x, (kt0 + t) * 128, mt * BN, &xfull[xs]);
+                    }
+                    if (++xs == C::kXStages) { xs = 0; xph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1 || warp == 14) {
+        // ===================== MMA issuers (one thread each). Issuer j takes the steps of a segment
+        // with local index % kIssuers == j, accumulating into its own TMEM accumulator. It waits only
+        // on afull[x]: the dequant warps arrive there after acquiring xfull[x], so the TMA-written
+        // activation tile of slot x is visible through that release/acquire chain.
+        const int j = (warp == 1) ? 0 : 1;
+        if (j < C::kIssuers) {   // whole warp runs the loop (warp-uniform descriptors); one lane issues
             const uint32_t idesc = idesc_i8(128, BN, /*a_signed=*/p.tx == nullptr);
             SegIter si(p);
-            int tile, k0, k1, stage = 0, ast = 0, cst = 0;
-            uint32_t phase = 0, aph = 0, cph = 0;
-            while (si.next(tile, k0, k1)) {
+            int tile, s0, s1, cst = 0, it0 = 0;
+            uint32_t cph = 0;
+            while (si.next(tile, s0, s1)) {
                 mbar_wait(&accempty[cst], cph ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem + kAStages * 32 + cst * BN;
-                for (int kt = k0; kt < k1; ++kt) {
-                    mbar_wait(&full[stage], phase);
-                    mbar_wait(&afull[ast], aph);
+                const uint32_t d = tmem + C::kAStages * 64 + (cst * C::kIssuers + j) * BN;
+                for (int local = j; local < s1 - s0; local += C::kIssuers) {
+                    const int it = it0 + local, sg = s0 + local;
+                    const int xs = it % C::kXStages, as = it % C::kAStages;
+                    const uint32_t xph = (uint32_t)(it / C::kXStages) & 1u, aph = (uint32_t)(it / C::kAStages) & 1u;
+                    const int nk = (2 * sg + 1 < p.KT) ? 2 : 1;
+                    if (lane == 0) QOQ_TRACE_IT(p, it, 4);
+                    mbar_wait(&afull[as], aph);
+                    mbar_wait(&xfull[xs], xph);
+                    if (lane == 0) QOQ_TRACE_IT(p, it, 5);
                     tc_fence_after();
-                    const uint32_t a = tmem + ast * 32;
-                    const uint32_t sb = smem_u32(smem + stage * C::kStageBytes);
+                    const uint32_t a = tmem + as * 64;
+                    const uint32_t sb = smem_u32(smem + C::kXOff + xs * C::kXStageBytes);
+                    if (elect_one()) {
+                        for (int t = 0; t < nk; ++t) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        mma_i8_ts(d, a + kk * 8, smem_desc_sw128(sb + kk * 32), idesc, (kt > k0 || kk > 0) ? 1u : 0u);
-                    tc_commit(&empty[stage]);    // activation tile consumed
-                    tc_commit(&aempty[ast]);     // expanded weight buffer consumed
-                    if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-                    if (++ast == kAStages) { ast = 0; aph ^= 1; }
+                            for (int kk = 0; kk < 4; ++kk) {
+                                mma_i8_ts(d, a + t * 32 + kk * 8, smem_desc_sw128(sb + t * C::kActBytes + kk * 32), idesc,
+                                          (local >= C::kIssuers || t > 0 || kk > 0) ? 1u : 0u);
+                                if (p.trace && blockIdx.x == 0 && it < 16)
+                                    p.trace[148 * 16 + 64 * 8 + it * 8 + t * 4 + kk] = clock64();
+                            }
+                        }
+                        tc_commit(&aempty[as]);      // expanded weight buffer consumed
+                        tc_commit(&xempty[xs]);      // activation slot consumed
+                    }
+                    __syncwarp();
+                    if (lane == 0) QOQ_TRACE_IT(p, it, 6);
                 }
-                tc_commit(&accfull[cst]);        // accumulator tile complete
+                if (elect_one()) tc_commit(&accfull[cst]);   // this issuer's accumulator is final
+                __syncwarp();
+                if (j == 0 && lane == 0) QOQ_TRACE(p, 5);
+                it0 += s1 - s0;
                 if (++cst == C::kAccStages) { cst = 0; cph ^= 1; }
             }
         }
-    } else if (warp >= 4 && warp < 8) {
-        // ===================== dequant: u4 -> (q̂ + 128) lanes -> TMEM A buffer
-        const int q = warp - 4;                       // TMEM lane quarter this warp may access
+    } else if (warp >= 2 && warp < 10) {
+        // ===================== dequant: u4 -> (q̂ + 128) lanes -> TMEM buffer of the step's X slot
+        // Two 4-warp groups take alternate steps; in a group, warp (w & 3) owns TMEM lanes
+        // 32(w&3)..+31 and thread r expands weight row r of each k-tile (32 TMEM columns per tile).
+        const int q = warp & 3;                       // TMEM lane quarter this warp may access
+        const int grp = (warp - 2) >> 2;              // steps it with it % 2 == grp
         const int r = q * 32 + lane;                  // weight row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const uint32_t flip = (p.tx == nullptr) ? 0x80808080u : 0u;
+        const bool tw = (warp == 2 && lane == 0);
         SegIter si(p);
-        int tile, k0, k1, stage = 0, ast = 0;
-        uint32_t phase = 0, aph = 0;
-        while (si.next(tile, k0, k1)) {
-            for (int kt = k0; kt < k1; ++kt) {
-                mbar_wait(&full[stage], phase);
-                const uint8_t* w = smem + stage * C::kStageBytes + C::kActBytes;
-                const uint32_t s = w[8192 + r];
-                const uint32_t bias = (128u - (uint32_t)w[8320 + r]) * 0x01010101u;
-                uint4 v[4];
+        int tile, s0, s1, ws = 0, it = 0;
+        uint32_t wph = 0;
+        while (si.next(tile, s0, s1)) {
+            for (int sg = s0; sg < s1; ++sg, ++it) {
+                if ((it & 1) == grp) {
+                    const int nk = (2 * sg + 1 < p.KT) ? 2 : 1;
+                    mbar_wait(&wfull[ws], wph);
+                    if (tw) QOQ_TRACE_IT(p, it, 0);
+                    const uint8_t* wb = smem + C::kWOff + ws * C::kWStageBytes;
+                    uint4 v[2][4];
+                    uint32_t sc[2], bias[2];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) v[c] = *reinterpret_cast<const uint4*>(w + c * 2048 + r * 16);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[stage]);   // packed bytes now live in registers
-                uint32_t out[32];
+                    for (int t = 0; t < 2; ++t) {
+                        if (t < nk) {
+                            const uint8_t* w = wb + t * kTileBytes;
+                            sc[t] = w[8192 + r];
+                            bias[t] = (128u - (uint32_t)w[8320 + r]) * 0x01010101u;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const uint32_t wd[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t lo = wd[i] & 0x0F0F0F0Fu;          // k = 32c + 4i .. +3
-                        const uint32_t hi = (wd[i] >> 4) & 0x0F0F0F0Fu;   // k = 32c + 16 + 4i .. +3
-                        out[c * 8 + i] = (lo * s + bias) ^ flip;
-                        out[c * 8 + 4 + i] = (hi * s + bias) ^ flip;
-                    }
-                }
-                mbar_wait(&aempty[ast], aph ^ 1);
-                tc_fence_after();
-                tmem_st_32x32b_x32(tmem + lane_off + ast * 32, out);
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&afull[ast]);
-                if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-                if (++ast == kAStages) { ast = 0; aph ^= 1; }
-            }
-        }
-    } else if (warp >= 8) {
-        // ===================== epilogue
-        const int q = warp - 8;
-        const int r = q * 32 + lane;
-        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        SegIter si(p);
-        int tile, k0, k1, cst = 0;
-        uint32_t cph = 0;
-        while (si.next(tile, k0, k1)) {
-            const int nt = tile / p.MT, mt = tile % p.MT;
-            const int n = nt * 128 + r;
-            const int m0 = mt * BN;
-            const bool whole = (k0 == 0 && k1 == p.KT);
-            const float s0f = OUT_I32 ? 0.0f : __half2float(__ldg(p.s0 + n));
-            int32_t* wst = p.ws + (size_t)tile * 128 * BN;
-            mbar_wait(&accfull[cst], cph);
-            tc_fence_after();
-            const uint32_t d = tmem + lane_off + kAStages * 32 + cst * BN;
-#pragma unroll 1
-            for (int j0 = 0; j0 < BN; j0 += C::kChunk) {
-                uint32_t v[C::kChunk];
-                if constexpr (C::kChunk == 32) tmem_ld_32x32b_x32(d + j0, v);
-                else tmem_ld_32x32b_x16(d + j0, v);
-                tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < C::kChunk; ++i) {
-                    const int m = m0 + j0 + i;
-                    if (m < p.M) {
-                        int32_t a = (int32_t)v[i];
-                        if (whole) {
-                            if (p.tx) a -= 128 * __ldg(p.tx + m);
-                            store_out<BN, OUT_I32>(p, m, n, a, s0f);
-                        } else {
-                            atomicAdd(wst + (size_t)(j0 + i) * 128 + r, a);
+                            for (int c = 0; c < 4; ++c) v[t][c] = *reinterpret_cast<const uint4*>(w + c * 2048 + r * 16);
                         }
                     }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&wfree[ws]);      // packed bytes now live in registers
+                    if (tw) QOQ_TRACE_IT(p, it, 1);
+                    const int as = it % C::kAStages;
+                    const uint32_t aph = (uint32_t)(it / C::kAStages) & 1u;
+                    mbar_wait(&aempty[as], aph ^ 1);             // TMEM buffer free again
+                    if (tw) QOQ_TRACE_IT(p, it, 2);
+                    tc_fence_after();
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        if (t < nk) {
+                            uint32_t out[32];
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                const uint32_t wd[4] = {v[t][c].x, v[t][c].y, v[t][c].z, v[t][c].w};
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const uint32_t lo = wd[i] & 0x0F0F0F0Fu;          // k = 32c + 4i .. +3
+                                    const uint32_t hi = (wd[i] >> 4) & 0x0F0F0F0Fu;   // k = 32c + 16 + 4i .. +3
+                                    out[c * 8 + i] = (QOQ_ABLATE & 8) ? wd[i] : (lo * sc[t] + bias[t]) ^ flip;
+                                    out[c * 8 + 4 + i] = (QOQ_ABLATE & 8) ? wd[i] : (hi * sc[t] + bias[t]) ^ flip;
+                                }
+                            }
+                            tmem_st_32x32b_x32(tmem + lane_off + as * 64 + t * 32, out);
+                        }
+                    }
+                    tmem_wait_st();
+                    if (tw) QOQ_TRACE_IT(p, it, 3);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&afull[as]);
+                }
+                if (++ws == C::kWStages) { ws = 0; wph ^= 1; }
+            }
+        }
+    } else if (warp >= 10 && warp < 14) {
+        // ===================== epilogue (warps 10-13)
+        const int q = warp & 3;
+        const int r = q * 32 + lane;                  // TMEM lane = weight row within the tile
+        const int et = threadIdx.x - kEpiThread0;     // 0..127 for cooperative phases
+        const int g = et >> 5, l = et & 31;           // vector mapping: rows 4l..4l+3, tokens g, g+4, ...
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        pdl_wait();
+        SegIter si(p);
+        int tile, s0, s1, cst = 0;
+        uint32_t cph = 0;
+        while (si.next(tile, s0, s1)) {
+            const int nt = tile / p.MT, mt = tile % p.MT;
+            const int n0 = nt * 128, m0 = mt * BN;
+            const bool whole = (s0 == 0 && s1 == p.KS);
+            const bool two = (C::kIssuers == 2) && (s1 - s0 >= 2);   // second accumulator holds data
+            int32_t* wst = p.ws + (size_t)tile * 128 * BN;
+            for (int jj = et; jj < BN; jj += 128) {
+                const int m = m0 + jj;
+                sxs[jj] = (!OUT_I32 && m < p.M) ? __half2float(__ldg(p.sx + m)) : 0.0f;
+                txs[jj] = (p.tx && m < p.M) ? 128 * __ldg(p.tx + m) : 0;
+            }
+            float s0v[4] = {0.f, 0.f, 0.f, 0.f};
+            if constexpr (!OUT_I32) {
+                const uint2 u = __ldg(reinterpret_cast<const uint2*>(p.s0 + n0 + 4 * l));
+                const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+                const float2 a = __half22float2(h2[0]), b = __half22float2(h2[1]);
+                s0v[0] = a.x; s0v[1] = a.y; s0v[2] = b.x; s0v[3] = b.y;
+            }
+            named_bar_sync(1, 128);
+            mbar_wait(&accfull[cst], cph);
+            if (et == 0) QOQ_TRACE(p, 6);
+            tc_fence_after();
+            const uint32_t d = tmem + lane_off + C::kAStages * 64 + cst * C::kIssuers * BN;
+            if (clustered) {
+                // ---- cluster split-K: stage this CTA's partial (sum of both issuers' accumulators) in
+                // its now-idle X ring, then one bulk reduce-add into the leader's staging area.
+                int32_t* part = reinterpret_cast<int32_t*>(smem + C::kXOff);
+#pragma unroll 1
+                for (int ci = 0; ci < BN / C::kChunk; ++ci) {
+                    const int j0 = ci * C::kChunk;
+                    uint32_t v[C::kChunk];
+                    tmem_ld_chunk<BN>(d + j0, v);
+                    if (two) {
+                        uint32_t v2[C::kChunk];
+                        tmem_ld_chunk<BN>(d + BN + j0, v2);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < C::kChunk; ++i) v[i] += v2[i];
+                    } else {
+                        tmem_wait_ld();
+                    }
+#pragma unroll
+                    for (int i = 0; i < C::kChunk; ++i) part[(j0 + i) * 128 + r] = (int32_t)v[i];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&accempty[cst]);
+                fence_proxy_async_smem();
+                named_bar_sync(1, 128);
+                if (et == 0) {
+                    QOQ_TRACE(p, 7);
+                    bulk_reduce_add_s32_cluster(mapa_shared(smem_u32(stg), 0), part, BN * 128 * 4,
+                                                mapa_shared(smem_u32(red_full), 0));
+                }
+                if (leader) {
+                    mbar_wait(red_full, 0);
+#pragma unroll
+                    for (int jj = g; jj < BN; jj += 4) {
+                        const int m = m0 + jj;
+                        if (m < p.M)
+                            write_out4<OUT_I32>(p, m, n0 + 4 * l, *reinterpret_cast<const int4*>(stg + jj * 128 + 4 * l),
+                                                txs[jj], sxs[jj], s0v);
+                    }
+                    if (et == 0) QOQ_TRACE(p, 9);
+                }
+                if (++cst == C::kAccStages) { cst = 0; cph ^= 1; }
+                named_bar_sync(1, 128);
+                continue;
+            }
+#pragma unroll 1
+            for (int ci = 0; ci < BN / C::kChunk; ++ci) {
+                const int j0 = ci * C::kChunk;
+                int32_t* sb = stg + (ci & 1) * (C::kChunk * 128);
+                uint32_t v[C::kChunk];
+                tmem_ld_chunk<BN>(d + j0, v);
+                if (two) {
+                    uint32_t v2[C::kChunk];
+                    tmem_ld_chunk<BN>(d + BN + j0, v2);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < C::kChunk; ++i) v[i] += v2[i];
+                } else {
+                    tmem_wait_ld();
+                }
+                if (ci == BN / C::kChunk - 1) {          // accumulators fully read: hand TMEM back
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&accempty[cst]);
+                }
+                if (et == 0) bulk_wait_read<1>();        // staging buffer (ci & 1) no longer read by TMA
+                named_bar_sync(1, 128);
+#pragma unroll
+                for (int i = 0; i < C::kChunk; ++i) sb[i * 128 + r] = (int32_t)v[i];
+                if (!whole) {
+                    fence_proxy_async_smem();
+                    named_bar_sync(1, 128);
+                    if (et == 0) {
+                        bulk_reduce_add_s32(wst + (size_t)j0 * 128, sb, C::kStgBytes);
+                        bulk_commit();
+                    }
+                } else {
+                    named_bar_sync(1, 128);
+#pragma unroll
+                    for (int jj = g; jj < C::kChunk; jj += 4) {
+                        const int m = m0 + j0 + jj;
+                        if (m < p.M)
+                            write_out4<OUT_I32>(p, m, n0 + 4 * l, *reinterpret_cast<const int4*>(sb + jj * 128 + 4 * l),
+                                                txs[j0 + jj], sxs[j0 + jj], s0v);
+                    }
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&accempty[cst]);
             if (++cst == C::kAccStages) { cst = 0; cph ^= 1; }
             if (!whole) {
-                __threadfence();
-                named_bar_sync(1, 128);
-                if (r == 0) {
-                    const int prev = atomicAdd(p.counters + tile, k1 - k0);
-                    *fin_flag = (prev + (k1 - k0) == p.KT) ? 1 : 0;
+                if (et == 0) {
+                    bulk_wait<0>();                      // this CTA's partial tile is in L2
+                    fence_proxy_async_global();
+                    __threadfence();
+                    QOQ_TRACE(p, 7);
+                    const int prev = atomicAdd(p.counters + tile, s1 - s0);
+                    *fin_flag = (prev + (s1 - s0) == p.KS) ? 1 : 0;
                 }
                 named_bar_sync(1, 128);
                 if (*fin_flag) {   // last contributor: finish the tile and restore the zero workspace
                     __threadfence();
-                    for (int j = 0; j < BN; ++j) {
-                        const int m = m0 + j;
-                        if (m < p.M) {
-                            int32_t a = __ldcg(wst + (size_t)j * 128 + r);
-                            wst[(size_t)j * 128 + r] = 0;
-                            if (p.tx) a -= 128 * __ldg(p.tx + m);
-                            store_out<BN, OUT_I32>(p, m, n, a, s0f);
+#pragma unroll 1
+                    for (int jb = 0; jb < BN; jb += 4 * C::kFinU) {
+                        int4 acc[C::kFinU];
+#pragma unroll
+                        for (int u = 0; u < C::kFinU; ++u)
+                            acc[u] = ld_cg_v4(wst + (size_t)(jb + g + 4 * u) * 128 + 4 * l);
+#pragma unroll
+                        for (int u = 0; u < C::kFinU; ++u) {
+                            const int jj = jb + g + 4 * u;
+                            *reinterpret_cast<int4*>(wst + (size_t)jj * 128 + 4 * l) = make_int4(0, 0, 0, 0);
+                            if (m0 + jj < p.M) write_out4<OUT_I32>(p, m0 + jj, n0 + 4 * l, acc[u], txs[jj], sxs[jj], s0v);
                         }
                     }
-                    if (r == 0) p.counters[tile] = 0;
+                    if (et == 0) {
+                        p.counters[tile] = 0;
+                        QOQ_TRACE(p, 9);
+                    }
                 }
-                named_bar_sync(1, 128);
             }
+            named_bar_sync(1, 128);   // sxs / txs / staging / fin_flag reuse by the next segment
+            if (et == 0) QOQ_TRACE(p, 8);
         }
+        if (et == 0) bulk_wait<0>();
     }
 
     tc_fence_before();
     __syncthreads();
+    // mode 2: no CTA may exit while its partial is still being read by a bulk reduce (completion is
+    // only signalled at the leader), so the leader releases the cluster after red_full completed.
+    if (clustered) cluster_sync_all();
+    if (threadIdx.x == 0) QOQ_TRACE(p, 10);
     pdl_launch_dependents();
     if (warp == 1) {
         tc_fence_after();
@@ -336,6 +599,44 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+// Largest number of co-resident S-CTA clusters of the BN kernel (cached per (BN, S); immutable after).
+template <int BN>
+static int max_clusters(int S) {
+    static int cache[9] = {0};
+    if (S < 1 || S > 8) return 0;
+    if (cache[S] == 0) {
+        auto kern = w4a8_gemm_kernel<BN, false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmemBytes);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(S * 64);
+        cfg.blockDim = dim3(kThreads + 64);
+        cfg.dynamicSmemBytes = Cfg<BN>::kSmemBytes;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = S;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            n = -1;
+        }
+        cache[S] = n;
+    }
+    return cache[S];
+}
+
+static int max_clusters_bn(int BN, int S) {
+    switch (BN) {
+        case 16: return max_clusters<16>(S);
+        case 32: return max_clusters<32>(S);
+        case 64: return max_clusters<64>(S);
+        default: return 0;
+    }
+}
+
 GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     GemmPlan p{};
     p.BN = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
@@ -343,15 +644,37 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     p.NT = N / kTileN;
     p.KT = K / kTileK;
     p.T = p.MT * p.NT;
-    p.I = (long long)p.T * p.KT;
-    if (p.T >= num_sms) {
-        p.mode = 0;
-        p.G = num_sms;
+    p.KS = (p.KT + 1) / 2;
+    p.I = (long long)p.T * p.KS;
+    p.S = 1;
+    // debug override for planner experiments: QOQ_FORCE_MODE=0 (no split) / 1 (stream-K) / 2 (clusters)
+    const char* fm = getenv("QOQ_FORCE_MODE");
+    const int force = fm ? atoi(fm) : -1;
+    int S = 1;
+    if (p.BN <= 64 && p.T < num_sms && force != 0 && force != 1) {
+        // cluster split-K: S CTAs per output tile, reduced through DSMEM (no workspace)
+        S = num_sms / p.T;
+        if (S > 8) S = 8;
+        if (S > p.KS) S = p.KS;
+        while (S >= 2) {
+            const int mc = max_clusters_bn(p.BN, S);
+            if (mc < 0 || (long long)mc >= p.T) break;   // all T clusters co-resident (or query unavailable)
+            --S;
+        }
+    }
+    if (S >= 2) {
+        p.mode = 2;
+        p.S = S;
+        p.G = p.T * S;
         p.ws_bytes = 0;
-    } else {
+    } else if (force == 1 || (force != 0 && p.T < num_sms && p.BN > 64)) {
         p.mode = 1;
         p.G = (int)(p.I < num_sms ? p.I : num_sms);
         p.ws_bytes = (size_t)p.T * 128 * p.BN * 4 + (size_t)p.T * 4;
+    } else {
+        p.mode = 0;
+        p.G = p.T < num_sms ? p.T : num_sms;
+        p.ws_bytes = 0;
     }
     return p;
 }
@@ -385,20 +708,34 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     kp.M = a.M;
     kp.MT = pl.MT;
     kp.KT = pl.KT;
+    kp.KS = pl.KS;
     kp.T = pl.T;
     kp.G = pl.G;
     kp.mode = pl.mode;
+    kp.S = pl.S;
     kp.I = pl.I;
+    kp.trace = static_cast<unsigned long long*>(a.trace);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.G);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(kThreads + 64);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (pl.mode == 2) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = pl.S;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, tm, kp);
 }
 

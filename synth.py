@@ -85,3 +85,22 @@ QWEN15_72B = [("qkv", 24576, 8192, "col"), ("o", 8192, 8192, "row"),
               ("down", 8192, 24576, "row")]
 MODELS = {"llama3-8b": (LLAMA3_8B, 32), "llama2-70b": (LLAMA2_70B, 80),
           "qwen1.5-72b": (QWEN15_72B, 80)}
+
+
+# ---- device-side generators for the large benchmark stacks (torch's seeded Philox on the GPU;
+# same distributions as above; used by bench.py only, never as oracle inputs).
+
+def device_weights_fp16(N: int, K: int, gen, device, std_scale: float = 1.0):
+    import torch
+    w = torch.randn(N, K, generator=gen, device=device, dtype=torch.float32)
+    return (w * (std_scale / K ** 0.5)).half()
+
+
+def device_activations_fp16(M: int, K: int, gen, device, n_outlier: int | None = None,
+                            outlier_scale: float = 20.0):
+    import torch
+    x = torch.randn(M, K, generator=gen, device=device, dtype=torch.float32)
+    if M > 0 and K > 0:
+        idx = torch.as_tensor(outlier_channels(K, 0, n_outlier), device=device)
+        x[:, idx] *= outlier_scale
+    return x.half()

@@ -166,3 +166,22 @@ def test_linear_host_e2e(gpu_lib):
     gpu_lib.linear_host(Xh, to_dev(p_ref), to_dev(s0_ref), N, Yh, scratch)
     torch.cuda.synchronize()
     check_y(Yh, oracle.linear_rows(X, p_ref, s0_ref, N))
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("M,N,K", [(16, 256, 256), (1, 1280, 1024), (64, 512, 2048), (33, 384, 1152),
+                                   (64, 4096, 4096)])
+def test_gemm_all_planner_modes_bit_exact(gpu_lib, monkeypatch, mode, M, N, K):
+    """Every work decomposition (0: whole tiles, 1: stream-K with the global workspace, 2: S-CTA
+    cluster split-K reduced through DSMEM) gives the identical INT32 accumulators and Y."""
+    monkeypatch.setenv("QOQ_FORCE_MODE", mode)
+    W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=M + N + K + int(mode))
+    ws = gpu_lib.Workspace(dev())
+    acc = gpu_lib.w4a8_gemm_i32(to_dev(qx_ref), to_dev(tx_ref), to_dev(p_ref), N, workspace=ws)
+    acc_ref = oracle.acc_from_packed(qx_ref, p_ref, N, K)
+    assert np.array_equal(acc.cpu().numpy(), acc_ref)
+    Y = gpu_lib.w4a8_gemm(to_dev(qx_ref), to_dev(sx_ref), None, to_dev(p_ref), to_dev(s0_ref), N, workspace=ws)
+    check_y(Y, oracle.epilogue_f64(acc_ref, sx_ref, s0_ref))
+    torch.cuda.synchronize()
+    if ws.buf is not None:
+        assert int(ws.buf.count_nonzero()) == 0
