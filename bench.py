@@ -78,11 +78,17 @@ def load_traffic(config_key):
 
 # ------------------------------------------------------------------ model layout and TP sharding
 
-def layer_shapes(model, M, world, rank):
-    """Per-rank GEMM list of one layer: (name, N_r, K_r, kind, quant_group). Column-parallel layers
-    split N, row-parallel layers split K (both at 128 boundaries). quant_group names which
-    activation quantization feeds the GEMM (gate and up share one, as in Fig. 7)."""
+def model_shapes(model, fused=True):
     shapes, _ = synth.MODELS[model]
+    return synth.fuse_gate_up(shapes) if fused else shapes
+
+
+def layer_shapes(model, M, world, rank, fused=True):
+    """Per-rank GEMM list of one layer: (name, N_r, K_r, kind, quant_group). Column-parallel layers
+    split N (a fused gate_up shard holds the rank's gate rows and up rows), row-parallel layers split
+    K (both at 128 boundaries). quant_group names which activation quantization feeds the GEMM
+    (gate and up share one, as in Fig. 7)."""
+    shapes = model_shapes(model, fused)
     out = []
     for name, N, K, kind in shapes:
         if kind == "col":
@@ -91,15 +97,16 @@ def layer_shapes(model, M, world, rank):
         else:
             assert K % (128 * world) == 0
             Nr, Kr = N, K // world
-        qg = {"qkv": "attn_in", "o": "attn_out", "gate": "mlp_in", "up": "mlp_in", "down": "mlp_act"}[name]
+        qg = {"qkv": "attn_in", "o": "attn_out", "gate": "mlp_in", "up": "mlp_in", "gate_up": "mlp_in",
+              "down": "mlp_act"}[name]
         out.append((name, Nr, Kr, kind, qg))
     return out
 
 
-def step_work(model, M, layers, world):
+def step_work(model, M, layers, world, fused=True):
     """Whole-job algorithmic bytes / ops of one step (all ranks together)."""
     b = ops = 0
-    for name, N, K, kind in synth.MODELS[model][0]:
+    for name, N, K, kind in model_shapes(model, fused):
         b += gemm_bytes(M, N, K) * layers
         ops += gemm_ops(M, N, K) * layers
     shapes = {n: (N, K) for n, N, K, _ in synth.MODELS[model][0]}
@@ -220,7 +227,8 @@ def run_reference(args):
 
 def config_dict(args, world):
     layers = args.layers or synth.MODELS[args.model][1]
-    return {"workload": f"{args.model} decode linear stack: {layers} layers x (qkv, o, gate, up, down), "
+    proj = "qkv, o, gate, up, down" if getattr(args, "unfused_gate_up", False) else "qkv, o, gate_up (fused), down"
+    return {"workload": f"{args.model} decode linear stack: {layers} layers x ({proj}), "
                         f"M={args.M} tokens, W4A8 g128, per-token INT8 activations",
             "model_shapes": args.model, "M": args.M, "layers": layers, "group": 128,
             "parallelism": f"tp{world}" if world > 1 else "single",
@@ -243,6 +251,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="per-projection GEMM breakdown and M sweep")
+    ap.add_argument("--unfused-gate-up", action="store_true", help="run gate and up as two GEMMs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -264,7 +273,8 @@ def main():
     qoq.load()
     M = args.M
     layers = args.layers or synth.MODELS[args.model][1]
-    shapes = layer_shapes(args.model, M, world, rank)
+    fused = not args.unfused_gate_up
+    shapes = layer_shapes(args.model, M, world, rank, fused)
     stream = torch.cuda.Stream(dev)
 
     # ---- offline: pack every layer's weights on device (row a1), distinct per layer
@@ -352,7 +362,7 @@ def main():
         ms_gemm = timed(g_gemm, max(10, args.steps // 2), 2)
 
     ms_step = ms_total / args.steps
-    step_bytes, step_ops = step_work(args.model, M, layers, world)
+    step_bytes, step_ops = step_work(args.model, M, layers, world, fused)
     value = step_bytes / (ms_step * 1e-3) / 1e9
 
     # dominant kernel: the W4A8 GEMM (per-rank launches in the gemm-only graph)

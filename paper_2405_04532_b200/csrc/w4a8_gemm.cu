@@ -647,12 +647,24 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     p.KS = (p.KT + 1) / 2;
     p.I = (long long)p.T * p.KS;
     p.S = 1;
-    // debug override for planner experiments: QOQ_FORCE_MODE=0 (no split) / 1 (stream-K) / 2 (clusters)
+    // Decomposition policy (measured on B200, tools/mode_sweep.sh, Llama-3-8B decode shapes):
+    //  * T >= #SMs: whole tiles (mode 0).
+    //  * BN <= 32: S-CTA cluster split-K through DSMEM (mode 2) — the partial is only 8-16 KB/CTA.
+    //  * BN = 64: no split while K <= 3072 steps-worth (KS <= 24; the pipeline fill/drain per CTA
+    //    costs more than the idle SMs), stream-K with the L2 workspace (mode 1) for long K.
+    //  * BN >= 128 with T < #SMs: stream-K (mode 1).
+    // QOQ_FORCE_MODE=0/1/2 overrides (debug / tests).
     const char* fm = getenv("QOQ_FORCE_MODE");
     const int force = fm ? atoi(fm) : -1;
+    int want;
+    if (force >= 0 && force <= 2) want = force;
+    else if (p.T >= num_sms) want = 0;
+    else if (p.BN <= 32) want = 2;
+    else if (p.BN == 64) want = p.KS <= 24 ? 0 : 1;
+    else want = 1;
+    if (want == 2 && p.BN > 64) want = 1;   // the DSMEM reduction target holds at most 128 x 64 INT32
     int S = 1;
-    if (p.BN <= 64 && p.T < num_sms && force != 0 && force != 1) {
-        // cluster split-K: S CTAs per output tile, reduced through DSMEM (no workspace)
+    if (want == 2) {
         S = num_sms / p.T;
         if (S > 8) S = 8;
         if (S > p.KS) S = p.KS;
@@ -661,13 +673,14 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
             if (mc < 0 || (long long)mc >= p.T) break;   // all T clusters co-resident (or query unavailable)
             --S;
         }
+        if (S < 2) want = (p.KS <= 24) ? 0 : 1;
     }
-    if (S >= 2) {
+    if (want == 2) {
         p.mode = 2;
         p.S = S;
         p.G = p.T * S;
         p.ws_bytes = 0;
-    } else if (force == 1 || (force != 0 && p.T < num_sms && p.BN > 64)) {
+    } else if (want == 1) {
         p.mode = 1;
         p.G = (int)(p.I < num_sms ? p.I : num_sms);
         p.ws_bytes = (size_t)p.T * 128 * p.BN * 4 + (size_t)p.T * 4;

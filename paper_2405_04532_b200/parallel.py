@@ -1,0 +1,86 @@
+"""Megatron-style tensor parallelism for the W4A8 linear layers (north_star).
+
+  * column-parallel (qkv, gate/up): W split along N (output channels). Each rank holds rows
+    [r N/TP, (r+1) N/TP), quantizes the replicated X exactly as 1 GPU would, and produces its
+    N-slice of Y. No collective. The slice is bit-identical to the 1-GPU result (reading Q17).
+  * row-parallel (o, down): W split along K (input channels) at 128-group boundaries. Each rank's
+    input X_r is the K-shard of X (already sharded by the previous layer); it is quantized with a
+    per-rank per-token scale, the rank emits an fp16 partial Y_r = fp16(acc_r s_x^r s0), and the
+    partials are summed with ONE all-reduce over the TP group (NCCL over NVLink/NVSwitch on GPUs).
+
+Only sharding / reduction plumbing lives here; every arithmetic step of the path runs in the CUDA
+library (paper_2405_04532_b200). Functions that compute take the per-rank `linear` callable, so the
+same host logic is exercised by the gloo tests on CPU (tests/test_tp_gloo.py) and by bench.py on GPUs.
+"""
+from __future__ import annotations
+
+GROUP = 128
+
+
+def check_shardable(N: int, K: int, kind: str, world: int) -> None:
+    if kind == "col":
+        if N % (GROUP * world):
+            raise ValueError(f"column-parallel N={N} not divisible into {world} shards of 128-multiples")
+    elif kind == "row":
+        if K % (GROUP * world):
+            raise ValueError(f"row-parallel K={K} not divisible into {world} shards at group boundaries")
+    else:
+        raise ValueError(kind)
+
+
+def shard_bounds(total: int, rank: int, world: int) -> tuple[int, int]:
+    step = total // world
+    return rank * step, (rank + 1) * step
+
+
+def shard_weight(W, kind: str, rank: int, world: int):
+    """The rank's shard of an nn.Linear weight W[N][K] (any 2-D array/tensor supporting slicing)."""
+    N, K = W.shape
+    check_shardable(N, K, kind, world)
+    if kind == "col":
+        a, b = shard_bounds(N, rank, world)
+        return W[a:b]
+    a, b = shard_bounds(K, rank, world)
+    return W[:, a:b]
+
+
+TILE_BYTES = 8448
+
+
+def shard_packed(packed, s0, N: int, K: int, kind: str, rank: int, world: int):
+    """Shard an already-packed weight (quantize once, offline, then distribute). The tile stream is
+    [N/128][K/128][8448] (include/qoq_b200.h): a column shard is the contiguous block of its 128-row
+    tiles (+ its rows of s0); a row shard gathers, for every row block, the k-tiles of its K range
+    (s0 stays the full per-channel vector: level 1 is per output channel over ALL of K)."""
+    check_shardable(N, K, kind, world)
+    NT, KT = N // GROUP, K // GROUP
+    tiles = packed.reshape(NT, KT, TILE_BYTES)
+    if kind == "col":
+        a, b = shard_bounds(NT, rank, world)
+        return tiles[a:b].reshape(-1), s0[a * GROUP:b * GROUP]
+    a, b = shard_bounds(KT, rank, world)
+    sub = tiles[:, a:b]
+    sub = sub.contiguous() if hasattr(sub, "contiguous") else sub.copy()
+    return sub.reshape(-1), s0
+
+
+def shard_input(X, kind: str, rank: int, world: int):
+    """Column-parallel layers see the replicated X; row-parallel layers see the K-shard of X."""
+    if kind == "col":
+        return X
+    K = X.shape[1]
+    a, b = shard_bounds(K, rank, world)
+    return X[:, a:b]
+
+
+def tp_linear(X, W_shard, kind: str, linear, all_reduce, rank: int, world: int):
+    """One TP linear layer on this rank.
+
+    linear(X_r, W_shard) -> Y_r  (the rank-local W4A8 linear: quantize X_r per token + GEMM)
+    all_reduce(Y) -> in-place SUM over the TP group (row-parallel only)
+    Returns the rank's N-slice (col) or the full, reduced Y (row)."""
+    X_r = shard_input(X, kind, rank, world)
+    Y = linear(X_r, W_shard)
+    if kind == "row" and world > 1:
+        all_reduce(Y)
+    return Y

@@ -87,6 +87,18 @@ MODELS = {"llama3-8b": (LLAMA3_8B, 32), "llama2-70b": (LLAMA2_70B, 80),
           "qwen1.5-72b": (QWEN15_72B, 80)}
 
 
+def fuse_gate_up(shapes):
+    """gate and up share their input (FFN-1, Fig. 7): serving stacks run them as
+    one GEMM over the concatenated [gate; up] weight (N = 2 x intermediate). Same algorithmic bytes."""
+    out = []
+    for name, N, K, kind in shapes:
+        if name == "gate":
+            out.append(("gate_up", 2 * N, K, kind))
+        elif name != "up":
+            out.append((name, N, K, kind))
+    return out
+
+
 # ---- device-side generators for the large benchmark stacks (torch's seeded Philox on the GPU;
 # same distributions as above; used by bench.py only, never as oracle inputs).
 

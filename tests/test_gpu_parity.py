@@ -185,3 +185,27 @@ def test_gemm_all_planner_modes_bit_exact(gpu_lib, monkeypatch, mode, M, N, K):
     torch.cuda.synchronize()
     if ws.buf is not None:
         assert int(ws.buf.count_nonzero()) == 0
+
+
+def test_tp_shards_on_device(gpu_lib):
+    """TP on the CUDA path (one GPU, shards run sequentially): column shards of the packed stream
+    give bit-identical N-slices; row shards' INT32 accumulators (same q_x K-slices) sum exactly to
+    the full accumulator."""
+    from paper_2405_04532_b200 import parallel
+    M, N, K, world = 16, 512, 1024, 4
+    W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=21)
+    packed, s0 = to_dev(p_ref), to_dev(s0_ref)
+    qx, sx, tx = to_dev(qx_ref), to_dev(sx_ref), to_dev(tx_ref)
+    full_acc = gpu_lib.w4a8_gemm_i32(qx, tx, packed, N)
+    full_y = gpu_lib.w4a8_gemm(qx, sx, tx, packed, s0, N)
+    cols = []
+    for r in range(world):
+        p_r, s0_r = parallel.shard_packed(packed, s0, N, K, "col", r, world)
+        cols.append(gpu_lib.w4a8_gemm(qx, sx, tx, p_r.contiguous(), s0_r.contiguous(), N // world))
+    assert torch.equal(torch.cat(cols, dim=1), full_y)
+    tot = torch.zeros_like(full_acc)
+    for r in range(world):
+        p_r, _ = parallel.shard_packed(packed, s0, N, K, "row", r, world)
+        qx_r = parallel.shard_input(qx, "row", r, world).contiguous()
+        tot += gpu_lib.w4a8_gemm_i32(qx_r, None, p_r.contiguous(), N)
+    assert torch.equal(tot, full_acc)

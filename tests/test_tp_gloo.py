@@ -1,0 +1,146 @@
+"""Tensor-parallel host logic on CPU: world_size 2 over `gloo` (reading Q17).
+
+Per-rank math is the CPU oracle (the per-rank GEMM itself is parity-tested on the GPU); what is
+checked here is the sharding and the reduction:
+  * column-parallel: each rank's slice is bit-identical to the 1-GPU oracle result on that slice;
+  * row-parallel: the all-reduced fp16 partials match the fp64 sum of the per-rank exact results
+    within the north_star tolerance, and approximate the 1-GPU result.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2405_04532_b200 import parallel
+
+RTOL, ATOL = 2e-3, 1e-3
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_linear(X_r, shard):
+    """Rank-local W4A8 linear on the CPU oracle from a packed shard: quantize X_r per token, GEMM, fp16."""
+    packed, s0, N = shard
+    X = np.ascontiguousarray(X_r)
+    y = oracle.linear_rows(X, np.ascontiguousarray(packed), np.ascontiguousarray(s0), N)
+    return torch.from_numpy(y.astype(np.float16))
+
+
+def _packed_shard(W, kind, rank, world):
+    """Quantize the full weight once (oracle packer), then shard the packed stream."""
+    N, K = W.shape
+    packed, s0 = oracle.quantize_weights(W)
+    p_r, s0_r = parallel.shard_packed(packed, s0, N, K, kind, rank, world)
+    return p_r, s0_r, (N // world if kind == "col" else N)
+
+
+def _worker(rank, world, port, kind, M, N, K, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # TP weights scaled 1/4 (SURVEY §8(d) "Row-parallel TP parity: W ~ N(0, 1/(16K))")
+        W = synth.weights_fp16(N, K, seed=3, std_scale=0.25)
+        X = synth.activations_fp16(M, K, seed=3)
+        W_r = _packed_shard(W, kind, rank, world)
+
+        def all_reduce(Y):
+            dist.all_reduce(Y, op=dist.ReduceOp.SUM)
+
+        Y = parallel.tp_linear(X, W_r, kind, _oracle_linear, all_reduce, rank, world)
+        out_q.put((rank, Y.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(kind, M, N, K, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, M, N, K, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_shard_helpers():
+    W = np.arange(256 * 512).reshape(256, 512)
+    assert parallel.shard_weight(W, "col", 1, 2).shape == (128, 512)
+    assert parallel.shard_weight(W, "row", 1, 2).shape == (256, 256)
+    assert np.array_equal(parallel.shard_weight(W, "row", 1, 2), W[:, 256:])
+    with pytest.raises(ValueError):
+        parallel.shard_weight(W, "col", 0, 4)       # 256 / 4 = 64 is not a multiple of 128
+    with pytest.raises(ValueError):
+        parallel.check_shardable(1280, 8192, "row", 3)
+    # every Llama-2-70B / Qwen1.5-72B TP shard of BASELINE configs 3-4 is group-aligned
+    for model in ("llama2-70b", "qwen1.5-72b"):
+        for _, N, K, kind in synth.MODELS[model][0]:
+            for tp in (2, 4, 8):
+                parallel.check_shardable(N, K, kind, tp)
+
+
+def test_column_parallel_gloo_bit_identical_slices():
+    M, N, K = 8, 256, 256
+    res = _run("col", M, N, K)
+    W = synth.weights_fp16(N, K, seed=3, std_scale=0.25)
+    X = synth.activations_fp16(M, K, seed=3)
+    packed, s0 = oracle.quantize_weights(W)
+    full = _oracle_linear(X, (packed, s0, N)).numpy()
+    got = np.concatenate([res[0], res[1]], axis=1)
+    assert np.array_equal(got.view(np.uint16), full.view(np.uint16))
+
+
+def test_row_parallel_gloo_allreduce_within_tolerance():
+    M, N, K = 8, 128, 512
+    res = _run("row", M, N, K)
+    assert np.array_equal(res[0].view(np.uint16), res[1].view(np.uint16))   # all ranks agree
+    W = synth.weights_fp16(N, K, seed=3, std_scale=0.25)
+    X = synth.activations_fp16(M, K, seed=3)
+    ref = np.zeros((M, N))
+    for r in range(2):
+        p_r, s0_r, _ = _packed_shard(W, "row", r, 2)
+        Xr = parallel.shard_input(X, "row", r, 2)
+        ref += oracle.linear_rows(np.ascontiguousarray(Xr), p_r, s0_r, N)
+    y = res[0].astype(np.float64)
+    assert np.all(np.abs(y - ref) <= RTOL * np.abs(ref) + ATOL)
+    # Same quantized weights as 1 GPU; only the per-token activation scales are per-rank (Q17), so
+    # the TP result stays close to the 1-GPU layer and inside the float layer's envelope.
+    fl = X.astype(np.float64) @ W.astype(np.float64).T
+    packed, s0 = oracle.quantize_weights(W)
+    one = oracle.linear_rows(X, packed, s0, N)
+    assert np.linalg.norm(y - one) / np.linalg.norm(one) < 0.05
+    assert np.linalg.norm(y - fl) / np.linalg.norm(fl) < 0.2
+
+
+def test_packed_row_shards_sum_to_the_full_accumulator():
+    """With the per-rank activation quantization replaced by the 1-GPU q_x (a K-slice of it), the
+    INT32 partials of the row shards sum EXACTLY to the 1-GPU accumulators: the shard operation on
+    the tile stream loses nothing."""
+    M, N, K = 4, 256, 768
+    W = synth.weights_fp16(N, K, seed=5)
+    X = synth.activations_fp16(M, K, seed=5)
+    packed, s0 = oracle.quantize_weights(W)
+    qx, _, _ = oracle.quantize_activations(X)
+    full = oracle.acc_from_packed(qx, packed, N, K)
+    tot = np.zeros_like(full)
+    for r in range(3):
+        p_r, _ = parallel.shard_packed(packed, s0, N, K, "row", r, 3)
+        qx_r = np.ascontiguousarray(parallel.shard_input(qx, "row", r, 3))
+        tot += oracle.acc_from_packed(qx_r, p_r, N, K // 3)
+    assert np.array_equal(tot, full)
