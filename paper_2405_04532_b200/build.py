@@ -53,6 +53,10 @@ if __name__ == "__main__":
     extra = ["-Xptxas", "-v"] if "--ptxas" in sys.argv else []
     variant = ""
     for a in sys.argv[1:]:
+        if a.startswith("--variant="):   # --variant=name:-DFOO=1,-DBAR=2
+            name, flags = a.split("=", 1)[1].split(":", 1)
+            variant = name
+            extra += flags.split(",")
         if a.startswith("--ablate="):
             variant = "ablate" + a.split("=")[1]
             extra.append("-DQOQ_ABLATE=" + a.split("=")[1])

@@ -143,35 +143,68 @@ __global__ void __launch_bounds__(128) level2_pack_kernel(const __half* __restri
 
 // ------------------------------------------------------------------ activations
 
-__global__ void __launch_bounds__(256) quantize_act_kernel(const __half* __restrict__ X, int K, int ldx,
-                                                           int8_t* __restrict__ qx, __half* __restrict__ sx,
-                                                           int32_t* __restrict__ tx) {
+// One CTA per token row. The row (K <= 256 * 8 * kVec fp16) is read ONCE into registers, reduced
+// (amax), quantized from registers and summed; rows longer than the register budget take the
+// streaming path (second read hits L1/L2). PDL: the dependent GEMM is released at entry — its CTAs
+// launch on the SMs this small grid leaves free and start streaming their (static) weights while
+// this kernel runs; they read q_x only after griddepcontrol.wait.
+constexpr int kQThreads = 256;
+constexpr int kVec = 8;   // uint4 (8 halves) per thread kept in registers: K <= 16384
+
+__device__ __forceinline__ uint2 quant8(uint4 u, float s, int& t) {
+    const __half* h = reinterpret_cast<const __half*>(&u);
+    uint32_t w[2] = {0, 0};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int q = min(127, max(-127, (int)roundf(__fdiv_rn(__half2float(h[e]), s))));
+        t += q;
+        w[e >> 2] |= (uint32_t)(q & 0xff) << (8 * (e & 3));
+    }
+    return make_uint2(w[0], w[1]);
+}
+
+__global__ void __launch_bounds__(kQThreads) quantize_act_kernel(const __half* __restrict__ X, int K, int ldx,
+                                                                 int8_t* __restrict__ qx, __half* __restrict__ sx,
+                                                                 int32_t* __restrict__ tx) {
     __shared__ float redf[32];
     __shared__ int redi[32];
+    pdl_launch_dependents();
     pdl_wait();
     const int m = blockIdx.x;
     const uint4* row = reinterpret_cast<const uint4*>(X + (size_t)m * ldx);
+    uint2* out = reinterpret_cast<uint2*>(qx + (size_t)m * K);
     const int nv = K / 8;
+    int t = 0;
+    if (nv <= kQThreads * kVec) {
+        uint4 r[kVec];
+        float a = 0.0f;
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) {
+            const int i = threadIdx.x + j * kQThreads;
+            r[j] = (i < nv) ? __ldg(row + i) : make_uint4(0, 0, 0, 0);
+            a = amax8(r[j], a);
+        }
+        a = block_reduce_max(a, redf);
+        const __half sh = sym_scale(a, 127.0f);
+        const float s = __half2float(sh);
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) {
+            const int i = threadIdx.x + j * kQThreads;
+            if (i < nv) out[i] = quant8(r[j], s, t);
+        }
+        if (tx) t = block_reduce_sum(t, redi);
+        if (threadIdx.x == 0) {
+            sx[m] = sh;
+            if (tx) tx[m] = t;
+        }
+        return;
+    }
     float a = 0.0f;
     for (int i = threadIdx.x; i < nv; i += blockDim.x) a = amax8(__ldg(row + i), a);
     a = block_reduce_max(a, redf);
     const __half sh = sym_scale(a, 127.0f);
     const float s = __half2float(sh);
-    int t = 0;
-    uint2* out = reinterpret_cast<uint2*>(qx + (size_t)m * K);
-    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-        uint4 u = __ldg(row + i);
-        const __half* h = reinterpret_cast<const __half*>(&u);
-        uint32_t w[2] = {0, 0};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int q = min(127, max(-127, (int)roundf(__fdiv_rn(__half2float(h[e]), s))));
-            t += q;
-            w[e >> 2] |= (uint32_t)(q & 0xff) << (8 * (e & 3));
-        }
-        out[i] = make_uint2(w[0], w[1]);
-    }
-    pdl_launch_dependents();
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) out[i] = quant8(__ldg(row + i), s, t);
     if (tx) t = block_reduce_sum(t, redi);
     if (threadIdx.x == 0) {
         sx[m] = sh;
@@ -195,7 +228,7 @@ cudaError_t launch_quantize_activations(const void* X, int M, int K, int ldx, in
                                         int32_t* tx, cudaStream_t st, bool pdl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(M);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(kQThreads);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -57,7 +57,11 @@ struct Cfg {
     static constexpr int kChunk = BN < 32 ? BN : 32;                  // TMEM columns per epilogue tcgen05.ld
     static constexpr int kStgBytes = kChunk * 128 * 4;                // one INT32 staging buffer [kChunk][128]
     static constexpr int kEpiBytes = 2 * kStgBytes + BN * 8;          // 2 staging buffers + per-token s_x, 128 t_x
+#ifndef QOQ_ACC_STAGES
     static constexpr int kAccStages = (2 * kIssuers * BN + 4 * 64 <= 512) ? 2 : 1;
+#else
+    static constexpr int kAccStages = (QOQ_ACC_STAGES * kIssuers * BN + 4 * 64 <= 512) ? QOQ_ACC_STAGES : 1;
+#endif
     static constexpr int kAccCols = kAccStages * kIssuers * BN;
     // Three independent rings: W (packed weights, HBM-latency bound, SMEM), X (activation k-tiles,
     // L2-latency bound, SMEM) and A (expanded weights, 64 TMEM columns per step). (Loading weights
@@ -65,10 +69,14 @@ struct Cfg {
     // register loads stall at HBM latency with too few bytes in flight per SM.)
     static constexpr int kARaw = (512 - kAccCols) / 64;
     static constexpr int kAStages = kARaw > 6 ? 6 : kARaw;
+#ifndef QOQ_XSTAGES
     static constexpr int kXStages = BN <= 32 ? 8 : BN == 64 ? 6 : BN == 128 ? 3 : 2;
+#else
+    static constexpr int kXStages = BN <= 64 ? QOQ_XSTAGES : BN == 128 ? 3 : 2;
+#endif
     static constexpr int kWStageBytes = ((2 * kTileBytes + 1023) / 1024) * 1024;   // packed weights of one step
     static constexpr int kWRaw = (212 * 1024 - kEpiBytes - kXStages * kXStageBytes) / kWStageBytes;
-    static constexpr int kWStages = kWRaw > 8 ? 8 : kWRaw;
+    static constexpr int kWStages = kWRaw > 12 ? 12 : kWRaw;
     static constexpr int kColsUsed = kAStages * 64 + kAccCols;
     static constexpr int kTmemCols = kColsUsed <= 32 ? 32 : kColsUsed <= 64 ? 64 : kColsUsed <= 128 ? 128
                                    : kColsUsed <= 256 ? 256 : 512;
@@ -127,6 +135,7 @@ struct SegIter {
             end = (long long)(b + 1) * p.I / p.G;
         }
     }
+    __device__ bool more() const { return mode == 0 ? (b + cur * G) < T : cur < end; }
     __device__ bool next(int& tile, int& s0, int& s1) {
         if (mode == 0) {
             const long long t = b + cur * G;
@@ -163,6 +172,28 @@ __device__ __forceinline__ void write_out4(const KParams& p, int m, int n, int4 
         u.x = *reinterpret_cast<uint32_t*>(&lo);
         u.y = *reinterpret_cast<uint32_t*>(&hi);
         *reinterpret_cast<uint2*>(static_cast<__half*>(p.out) + (size_t)m * p.ldo + n) = u;
+    }
+}
+
+// Expand one 128-weight row of a packed tile (4 x 16 B = 128 u4 codes) into 32 TMEM words of
+// four 8-bit lanes each: lane = q_u4 * s_u8 + (128 - z*s_u8) = q̂ + 128 ∈ [7, 254] (no cross-lane
+// carry: the protective range bounds q̂ to [-121, 126]). SIGNED additionally flips the
+// lane MSBs (XOR 0x80) to give q̂ as s8. Per 8 weights: 2 LOP3 (ALU pipe) + IMAD.HI (the >> 4, on
+// the FMA pipe) + 2 IMAD (FMA pipe) [+ 2 LOP3], balancing the two integer pipes.
+template <bool SIGNED>
+__device__ __forceinline__ void expand_row(const uint4 (&v)[4], uint32_t s, uint32_t bias, uint32_t (&out)[32]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint32_t wd[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t lo = wd[i] & 0x0F0F0F0Fu;                      // k = 32c + 4i .. +3
+            const uint32_t hi = __umulhi(wd[i], 0x10000000u) & 0x0F0F0F0Fu;   // (w >> 4): k = 32c + 16 + 4i ..
+            uint32_t a = lo * s + bias, b = hi * s + bias;
+            if (SIGNED) { a ^= 0x80808080u; b ^= 0x80808080u; }
+            out[c * 8 + i] = (QOQ_ABLATE & 8) ? wd[i] : a;
+            out[c * 8 + 4 + i] = (QOQ_ABLATE & 8) ? wd[i] : b;
+        }
     }
 }
 
@@ -340,6 +371,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
                 }
                 if (elect_one()) tc_commit(&accfull[cst]);   // this issuer's accumulator is final
                 __syncwarp();
+                if (!si.more()) pdl_launch_dependents();      // mainloop issued: let the next kernel launch
                 if (j == 0 && lane == 0) QOQ_TRACE(p, 5);
                 it0 += s1 - s0;
                 if (++cst == C::kAccStages) { cst = 0; cph ^= 1; }
@@ -353,7 +385,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
         const int grp = (warp - 2) >> 2;              // steps it with it % 2 == grp
         const int r = q * 32 + lane;                  // weight row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        const uint32_t flip = (p.tx == nullptr) ? 0x80808080u : 0u;
+        const bool signed_a = (p.tx == nullptr);   // no t_x: feed s8 lanes (XOR), else biased u8
         const bool tw = (warp == 2 && lane == 0);
         SegIter si(p);
         int tile, s0, s1, ws = 0, it = 0;
@@ -389,18 +421,13 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
                     for (int t = 0; t < 2; ++t) {
                         if (t < nk) {
                             uint32_t out[32];
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) {
-                                const uint32_t wd[4] = {v[t][c].x, v[t][c].y, v[t][c].z, v[t][c].w};
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    const uint32_t lo = wd[i] & 0x0F0F0F0Fu;          // k = 32c + 4i .. +3
-                                    const uint32_t hi = (wd[i] >> 4) & 0x0F0F0F0Fu;   // k = 32c + 16 + 4i .. +3
-                                    out[c * 8 + i] = (QOQ_ABLATE & 8) ? wd[i] : (lo * sc[t] + bias[t]) ^ flip;
-                                    out[c * 8 + 4 + i] = (QOQ_ABLATE & 8) ? wd[i] : (hi * sc[t] + bias[t]) ^ flip;
-                                }
-                            }
+                            if (signed_a) expand_row<true>(v[t], sc[t], bias[t], out);
+                            else expand_row<false>(v[t], sc[t], bias[t], out);
+                            if (tw && p.trace && blockIdx.x == 0 && it < 16)
+                                p.trace[148 * 16 + 64 * 8 + 16 * 8 + it * 8 + 2 * t] = clock64();
                             tmem_st_32x32b_x32(tmem + lane_off + as * 64 + t * 32, out);
+                            if (tw && p.trace && blockIdx.x == 0 && it < 16)
+                                p.trace[148 * 16 + 64 * 8 + 16 * 8 + it * 8 + 2 * t + 1] = clock64();
                         }
                     }
                     tmem_wait_st();

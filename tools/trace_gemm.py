@@ -44,7 +44,7 @@ def main():
     Y = torch.empty(a.M, a.N, dtype=torch.float16, device=dev)
     wsb = qoq.gemm_workspace_bytes(a.M, a.N, a.K)
     ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=dev)
-    tr = torch.zeros(148 * 16 + 64 * 8 + 16 * 8, dtype=torch.int64, device=dev)
+    tr = torch.zeros(148 * 16 + 64 * 8 + 16 * 8 * 2, dtype=torch.int64, device=dev)
     s = torch.cuda.current_stream()
     for rep in range(3):
         for p, s0 in packs:
@@ -56,7 +56,8 @@ def main():
     full = tr.cpu().numpy().astype(np.float64)
     t = full[:148 * 16].reshape(-1, 16)
     its = full[148 * 16:148 * 16 + 512].reshape(64, 8)
-    mm = full[148 * 16 + 512:].reshape(16, 8)
+    mm = full[148 * 16 + 512:148 * 16 + 640].reshape(16, 8)
+    dq = full[148 * 16 + 640:].reshape(16, 8)
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
     rel = np.where(t > 0, t - t0, np.nan)
@@ -80,6 +81,11 @@ def main():
     for i in range(16):
         if its[i, 5] > 0 and mm[i, 0] > 0:
             print(f"   it{i:2d} " + " ".join(f"{int(v - its[i, 5]):6d}" for v in mm[i] if v > 0))
+    print("  CTA 0 dequant detail (cycles after xready): comp0 st0_issued comp1 st1_issued | wait_st_done")
+    for i in range(16):
+        if its[i, 2] > 0 and dq[i, 0] > 0:
+            print(f"   it{i:2d} " + " ".join(f"{int(v - its[i, 2]):6d}" for v in dq[i, :4] if v > 0)
+                  + f" | {int(its[i, 3] - its[i, 2]):6d}")
 
 
 if __name__ == "__main__":
