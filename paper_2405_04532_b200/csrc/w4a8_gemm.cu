@@ -40,9 +40,18 @@
 
 namespace qoq {
 
+#ifndef QOQ_DEQ_GROUPS
+#define QOQ_DEQ_GROUPS 2
+#endif
+constexpr int kDeqGroups = QOQ_DEQ_GROUPS;   // 4-warp dequant groups taking steps round-robin
+constexpr int kDeqWarp1 = 2 + 4 * kDeqGroups;        // first warp after the dequant warps
+constexpr int kEpiWarp0 = kDeqWarp1;                 // epilogue: 4 warps
+constexpr int kMma1Warp = kEpiWarp0 + 4;             // MMA issuer 1
+constexpr int kXProdWarp = kMma1Warp + 1;            // activation producer
+constexpr int kBlockThreads = 32 * (kXProdWarp + 1);
 constexpr int kThreads = 448;       // + 64 below: warps 0 weight producer, 1 MMA issuer 0 + TMEM owner,
                                     // 2-9 dequant, 10-13 epilogue, 14 MMA issuer 1, 15 activation producer
-constexpr int kEpiThread0 = 320;    // first epilogue thread (warps 10-13)
+constexpr int kEpiThread0 = 32 * kEpiWarp0;   // first epilogue thread
 
 // One pipeline STEP = up to two consecutive 128-deep k-tiles of one output tile: the handoff
 // (dequant -> MMA, MMA -> producer) is amortized over 8 MMAs, and two MMA-issuing warps take
@@ -67,16 +76,22 @@ struct Cfg {
     // L2-latency bound, SMEM) and A (expanded weights, 64 TMEM columns per step). (Loading weights
     // straight from L2 into registers after a bulk L2 prefetch was measured slower on B200: the
     // register loads stall at HBM latency with too few bytes in flight per SM.)
-    static constexpr int kARaw = (512 - kAccCols) / 64;
-    static constexpr int kAStages = kARaw > 6 ? 6 : kARaw;
+    // Ring depths are multiples of the number of roles that take turns on them (dequant groups on
+    // W and A, the two MMA issuers on A and X), so every slot is always consumed by the same role
+    // and no waiter can run two mbarrier phases ahead (parity waits would alias).
+    static constexpr int kARot = kDeqGroups % 2 == 0 ? kDeqGroups : 2 * kDeqGroups;   // lcm(2, groups)
+    static constexpr int kARaw0 = (512 - kAccCols) / 64;
+    static constexpr int kARaw = kARaw0 > 6 ? 6 : kARaw0;
+    static constexpr int kAStages = (kARaw / kARot) * kARot;
 #ifndef QOQ_XSTAGES
-    static constexpr int kXStages = BN <= 32 ? 8 : BN == 64 ? 6 : BN == 128 ? 3 : 2;
+    static constexpr int kXStages = BN <= 32 ? 8 : BN == 64 ? 6 : 2;
 #else
-    static constexpr int kXStages = BN <= 64 ? QOQ_XSTAGES : BN == 128 ? 3 : 2;
+    static constexpr int kXStages = BN <= 64 ? QOQ_XSTAGES : 2;
 #endif
     static constexpr int kWStageBytes = ((2 * kTileBytes + 1023) / 1024) * 1024;   // packed weights of one step
     static constexpr int kWRaw = (212 * 1024 - kEpiBytes - kXStages * kXStageBytes) / kWStageBytes;
-    static constexpr int kWStages = kWRaw > 12 ? 12 : kWRaw;
+    static constexpr int kWCap = kWRaw > 12 ? 12 : kWRaw;
+    static constexpr int kWStages = (kWCap / kDeqGroups) * kDeqGroups;
     static constexpr int kColsUsed = kAStages * 64 + kAccCols;
     static constexpr int kTmemCols = kColsUsed <= 32 ? 32 : kColsUsed <= 64 ? 64 : kColsUsed <= 128 ? 128
                                    : kColsUsed <= 256 ? 256 : 512;
@@ -88,6 +103,7 @@ struct Cfg {
     static constexpr int kSmemBytes = 1024 + kBarOff + kBarBytes;
     static constexpr int kFinU = BN / 4 < 8 ? BN / 4 : 8;             // independent 16-B loads per finalize batch
     static_assert(kXStages >= 2 && kWStages >= 2 && kAStages >= 2, "pipeline too shallow");
+    static_assert(kXStages % kIssuers == 0 && kWStages % kDeqGroups == 0 && kAStages % kARot == 0, "ring rotation");
     static_assert(kColsUsed <= 512, "TMEM overflow");
     static_assert(kSmemBytes <= 227 * 1024, "SMEM overflow");
 };
@@ -204,7 +220,7 @@ __device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<
 }
 
 template <int BN, bool OUT_I32>
-__global__ void __launch_bounds__(kThreads + 64, 1)
+__global__ void __launch_bounds__(kBlockThreads, 1)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
@@ -300,7 +316,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
                 }
             }
         }
-    } else if (warp == 15) {
+    } else if (warp == kXProdWarp) {
         // ===================== activation producer: TMA 2-D (SWIZZLE_128B) k-tiles of q_x
         if (lane == 0) {
             pdl_wait();
@@ -326,7 +342,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
                 }
             }
         }
-    } else if (warp == 1 || warp == 14) {
+    } else if (warp == 1 || warp == kMma1Warp) {
         // ===================== MMA issuers (one thread each). Issuer j takes the steps of a segment
         // with local index % kIssuers == j, accumulating into its own TMEM accumulator. It waits only
         // on afull[x]: the dequant warps arrive there after acquiring xfull[x], so the TMA-written
@@ -341,7 +357,10 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
                 mbar_wait(&accempty[cst], cph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + C::kAStages * 64 + (cst * C::kIssuers + j) * BN;
-                for (int local = j; local < s1 - s0; local += C::kIssuers) {
+                // issuer j takes the steps with GLOBAL index it % kIssuers == j (so each X slot / A
+                // buffer is always consumed by the same issuer); first own step zero-initializes
+                const int first = (j - it0 % C::kIssuers + C::kIssuers) % C::kIssuers;
+                for (int local = first; local < s1 - s0; local += C::kIssuers) {
                     const int it = it0 + local, sg = s0 + local;
                     const int xs = it % C::kXStages, as = it % C::kAStages;
                     const uint32_t xph = (uint32_t)(it / C::kXStages) & 1u, aph = (uint32_t)(it / C::kAStages) & 1u;
@@ -358,7 +377,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
                                 mma_i8_ts(d, a + t * 32 + kk * 8, smem_desc_sw128(sb + t * C::kActBytes + kk * 32), idesc,
-                                          (local >= C::kIssuers || t > 0 || kk > 0) ? 1u : 0u);
+                                          (local > first || t > 0 || kk > 0) ? 1u : 0u);
                                 if (p.trace && blockIdx.x == 0 && it < 16)
                                     p.trace[148 * 16 + 64 * 8 + it * 8 + t * 4 + kk] = clock64();
                             }
@@ -377,12 +396,12 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
                 if (++cst == C::kAccStages) { cst = 0; cph ^= 1; }
             }
         }
-    } else if (warp >= 2 && warp < 10) {
+    } else if (warp >= 2 && warp < kDeqWarp1) {
         // ===================== dequant: u4 -> (q̂ + 128) lanes -> TMEM buffer of the step's X slot
         // Two 4-warp groups take alternate steps; in a group, warp (w & 3) owns TMEM lanes
         // 32(w&3)..+31 and thread r expands weight row r of each k-tile (32 TMEM columns per tile).
         const int q = warp & 3;                       // TMEM lane quarter this warp may access
-        const int grp = (warp - 2) >> 2;              // steps it with it % 2 == grp
+        const int grp = (warp - 2) >> 2;              // steps it with it % kDeqGroups == grp
         const int r = q * 32 + lane;                  // weight row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const bool signed_a = (p.tx == nullptr);   // no t_x: feed s8 lanes (XOR), else biased u8
@@ -392,7 +411,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
         uint32_t wph = 0;
         while (si.next(tile, s0, s1)) {
             for (int sg = s0; sg < s1; ++sg, ++it) {
-                if ((it & 1) == grp) {
+                if (it % kDeqGroups == grp) {
                     const int nk = (2 * sg + 1 < p.KT) ? 2 : 1;
                     mbar_wait(&wfull[ws], wph);
                     if (tw) QOQ_TRACE_IT(p, it, 0);
@@ -439,7 +458,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
                 if (++ws == C::kWStages) { ws = 0; wph ^= 1; }
             }
         }
-    } else if (warp >= 10 && warp < 14) {
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ===================== epilogue (warps 10-13)
         const int q = warp & 3;
         const int r = q * 32 + lane;                  // TMEM lane = weight row within the tile
@@ -448,11 +467,14 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         pdl_wait();
         SegIter si(p);
-        int tile, s0, s1, cst = 0;
+        int tile, s0, s1, cst = 0, it0e = 0;
         uint32_t cph = 0;
         while (si.next(tile, s0, s1)) {
             const int nt = tile / p.MT, mt = tile % p.MT;
             const int n0 = nt * 128, m0 = mt * BN;
+            // a 1-step segment lives in the accumulator of the issuer that owns that global step
+            const int single = (C::kIssuers == 2 && s1 - s0 == 1) ? (it0e % 2) : 0;
+            it0e += s1 - s0;
             const bool whole = (s0 == 0 && s1 == p.KS);
             const bool two = (C::kIssuers == 2) && (s1 - s0 >= 2);   // second accumulator holds data
             int32_t* wst = p.ws + (size_t)tile * 128 * BN;
@@ -472,7 +494,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1)
             mbar_wait(&accfull[cst], cph);
             if (et == 0) QOQ_TRACE(p, 6);
             tc_fence_after();
-            const uint32_t d = tmem + lane_off + C::kAStages * 64 + cst * C::kIssuers * BN;
+            const uint32_t d = tmem + lane_off + C::kAStages * 64 + (cst * C::kIssuers + single) * BN;
             if (clustered) {
                 // ---- cluster split-K: stage this CTA's partial (sum of both issuers' accumulators) in
                 // its now-idle X ring, then one bulk reduce-add into the leader's staging area.
@@ -636,7 +658,7 @@ static int max_clusters(int S) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmemBytes);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(S * 64);
-        cfg.blockDim = dim3(kThreads + 64);
+        cfg.blockDim = dim3(kBlockThreads);
         cfg.dynamicSmemBytes = Cfg<BN>::kSmemBytes;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -757,7 +779,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     kp.trace = static_cast<unsigned long long*>(a.trace);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.G);
-    cfg.blockDim = dim3(kThreads + 64);
+    cfg.blockDim = dim3(kBlockThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];

@@ -209,3 +209,25 @@ def test_tp_shards_on_device(gpu_lib):
         qx_r = parallel.shard_input(qx, "row", r, world).contiguous()
         tot += gpu_lib.w4a8_gemm_i32(qx_r, None, p_r.contiguous(), N)
     assert torch.equal(tot, full_acc)
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("M,N,K", [
+    (16, 19200, 640),    # BN=16: 150 tiles > 148 SMs (persistent CTAs own 2 tiles), KS=3 (odd)
+    (5, 2560, 1408),     # BN=16: KT=11 -> last step holds one k-tile; odd-length stream-K segments
+    (40, 1280, 3200),    # BN=64: KS=13
+    (64, 19200, 384),    # BN=64: 150 tiles, KS=2 with a 1-tile last step
+    (100, 1280, 1664),   # BN=128: KS=7
+    (200, 768, 2688),    # BN=256: one issuer, KS=11
+])
+def test_gemm_segment_edge_cases_bit_exact(gpu_lib, monkeypatch, mode, M, N, K):
+    """Odd step counts, 1-tile last steps, multi-tile persistent CTAs and odd-length split-K
+    segments in every decomposition: the pipeline rings and the two MMA issuers' accumulators must
+    still give the exact INT32 sums."""
+    monkeypatch.setenv("QOQ_FORCE_MODE", mode)
+    W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=M + K)
+    for use_tx in (True, False):
+        acc = gpu_lib.w4a8_gemm_i32(to_dev(qx_ref), to_dev(tx_ref) if use_tx else None, to_dev(p_ref), N)
+        acc_ref = oracle.acc_from_packed(qx_ref, p_ref, N, K)
+        a = acc.cpu().numpy()
+        assert np.array_equal(a, acc_ref), f"{(a != acc_ref).sum()} accumulators differ (tx={use_tx})"
