@@ -22,6 +22,7 @@ struct GemmPlan {
     int G;           // CTAs (persistent, <= #SMs)
     int mode;        // 0: whole tiles round-robin; 1: stream-K (global workspace); 2: S-CTA cluster split-K
     int S;           // mode 2: CTAs (cluster size) per output tile
+    int CG;          // 1, or 2: CTA pairs (cta_group::2); then T counts tile pairs and G pairs
     size_t ws_bytes; // INT32 partials + per-tile counters (mode 1), else 0
 };
 

@@ -58,10 +58,16 @@ constexpr int kEpiThread0 = 32 * kEpiWarp0;   // first epilogue thread
 // alternate steps of a segment into separate accumulators (summed in the epilogue). Measured on
 // B200 (tools/mma_bench2.cu): one issuer, one tile per handoff ~520 cycles per 128x128 tile; two
 // issuers, two tiles per handoff ~193 cycles (MMA floor at N <= 64: 4 x 45 cycles).
-template <int BN>
+// CG = 1: one CTA owns a 128-row weight tile (tcgen05 cta_group::1, MMA M = 128).
+// CG = 2: a CTA pair (cluster of 2) owns two 128-row tiles; each CTA expands its own tile into its
+// own TMEM and holds half of the activation rows; the leader issues cta_group::2 MMAs (M = 256) —
+// half the MMA instructions, handoffs and activation SMEM traffic per SM (tools/cta2_check.cu:
+// 32 cycles per 256x64x32 MMA vs 45.5 per 128x64x32 on one SM).
+template <int BN, int CG = 1>
 struct Cfg {
     static constexpr int kIssuers = BN <= 128 ? 2 : 1;
-    static constexpr int kActBytes = BN * 128;                        // one k-tile of activations
+    static constexpr int kActRows = BN / CG;                          // activation rows held by this CTA
+    static constexpr int kActBytes = kActRows * 128;                  // one k-tile of this CTA's activations
     static constexpr int kXStageBytes = 2 * kActBytes;                // activations of one step (1024-aligned)
     static constexpr int kChunk = BN < 32 ? BN : 32;                  // TMEM columns per epilogue tcgen05.ld
     static constexpr int kStgBytes = kChunk * 128 * 4;                // one INT32 staging buffer [kChunk][128]
@@ -138,7 +144,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct SegIter {
     long long cur, end;
     int b, G, KS, T, mode;
-    __device__ SegIter(const KParams& p) : b(blockIdx.x), G(p.G), KS(p.KS), T(p.T), mode(p.mode) {
+    __device__ SegIter(const KParams& p, int cg = 1) : b(blockIdx.x / cg), G(p.G), KS(p.KS), T(p.T), mode(p.mode) {
         if (mode == 0) {
             cur = 0;
             end = 0;
@@ -214,15 +220,15 @@ __device__ __forceinline__ void expand_row(const uint4 (&v)[4], uint32_t s, uint
 }
 
 template <int BN>
-__device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<BN>::kChunk]) {
+__device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<BN, 1>::kChunk]) {
     if constexpr (Cfg<BN>::kChunk == 32) tmem_ld_32x32b_x32(taddr, v);
     else tmem_ld_32x32b_x16(taddr, v);
 }
 
-template <int BN, bool OUT_I32>
+template <int BN, bool OUT_I32, int CG>
 __global__ void __launch_bounds__(kBlockThreads, 1)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B aligned base derived by pointer arithmetic on the __shared__ array, so the compiler keeps
     // the shared address space (LDS/STS, not generic LD/ST) for everything carved from it
@@ -247,6 +253,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     if (threadIdx.x == 0) QOQ_TRACE(p, 0);
     const bool clustered = (p.mode == 2);
     const bool leader = clustered && cluster_ctarank() == 0;
+    const int rank = (CG == 2) ? (int)cluster_ctarank() : 0;   // CTA-pair: which 128-row tile of the pair
     if (leader) {   // zero the reduction target (the epilogue staging area) for the bulk reduce-adds
         for (int i = threadIdx.x; i < BN * 128; i += blockDim.x) stg[i] = 0;
         fence_proxy_async_smem();
@@ -267,23 +274,30 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
             mbar_init(&xempty[i], 1);
         }
         for (int i = 0; i < C::kAStages; ++i) {
-            mbar_init(&afull[i], 4);
+            mbar_init(&afull[i], 4 * CG);     // CG = 2: the peer's dequant warps arrive remotely on the leader's
             mbar_init(&aempty[i], 1);
         }
         for (int i = 0; i < C::kAccStages; ++i) {
             mbar_init(&accfull[i], C::kIssuers);
-            mbar_init(&accempty[i], 4);
+            mbar_init(&accempty[i], 4 * CG);  // CG = 2: both CTAs' epilogues free the pair's accumulators
         }
         fence_mbar_init();
         prefetch_tmap(&tmap_x);
     }
     if (warp == 1) {
-        tmem_alloc(tmem_slot, C::kTmemCols);
-        tmem_relinquish();
+        if constexpr (CG == 2) {
+            tmem_alloc2(tmem_slot, C::kTmemCols);
+            tmem_relinquish2();
+        } else {
+            tmem_alloc(tmem_slot, C::kTmemCols);
+            tmem_relinquish();
+        }
     }
     tc_fence_before();
     __syncthreads();
-    if (clustered) cluster_sync_all();   // leader's zeroed target + armed red_full visible cluster-wide
+    // mode 2: leader's zeroed target + armed red_full visible cluster-wide; CG = 2: the pair's
+    // barriers initialized before any remote arrive
+    if (clustered || CG == 2) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) QOQ_TRACE(p, 1);
@@ -296,11 +310,11 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
         // Weights are static, so it runs ahead of griddepcontrol.wait (overlaps the previous kernel).
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();   // each weight byte is read once
-            SegIter si(p);
+            SegIter si(p, CG);
             int tile, s0, s1, ws = 0;
             uint32_t wph = 0;
             while (si.next(tile, s0, s1)) {
-                const int nt = tile / p.MT;
+                const int nt = (tile / p.MT) * CG + rank;
                 for (int sg = s0; sg < s1; ++sg) {
                     const int kt0 = 2 * sg, nk = (kt0 + 1 < p.KT) ? 2 : 1;
                     mbar_wait(&wfree[ws], wph ^ 1);
@@ -321,11 +335,12 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
         if (lane == 0) {
             pdl_wait();
             QOQ_TRACE(p, 2);
-            SegIter si(p);
+            SegIter si(p, CG);
             int tile, s0, s1, xs = 0, it = 0;
             uint32_t xph = 0;
             while (si.next(tile, s0, s1)) {
                 const int mt = tile % p.MT;
+                const int row0 = mt * BN + rank * C::kActRows;   // CG = 2: this CTA's half of the tokens
                 for (int sg = s0; sg < s1; ++sg, ++it) {
                     const int kt0 = 2 * sg, nk = (kt0 + 1 < p.KT) ? 2 : 1;
                     mbar_wait(&xempty[xs], xph ^ 1);         // previous step of this slot consumed by the MMAs
@@ -336,7 +351,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                     } else {
                         mbar_arrive_expect_tx(&xfull[xs], nk * C::kActBytes);
                         for (int t = 0; t < nk; ++t)
-                            tma_load_2d(dst + t * C::kActBytes, &tmap_x, (kt0 + t) * 128, mt * BN, &xfull[xs]);
+                            tma_load_2d(dst + t * C::kActBytes, &tmap_x, (kt0 + t) * 128, row0, &xfull[xs]);
                     }
                     if (++xs == C::kXStages) { xs = 0; xph ^= 1; }
                 }
@@ -348,9 +363,9 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
         // on afull[x]: the dequant warps arrive there after acquiring xfull[x], so the TMA-written
         // activation tile of slot x is visible through that release/acquire chain.
         const int j = (warp == 1) ? 0 : 1;
-        if (j < C::kIssuers) {   // whole warp runs the loop (warp-uniform descriptors); one lane issues
-            const uint32_t idesc = idesc_i8(128, BN, /*a_signed=*/p.tx == nullptr);
-            SegIter si(p);
+        if (j < C::kIssuers && rank == 0) {   // whole warp runs the loop (warp-uniform descriptors); one lane issues
+            const uint32_t idesc = idesc_i8(128 * CG, BN, /*a_signed=*/p.tx == nullptr);
+            SegIter si(p, CG);
             int tile, s0, s1, cst = 0, it0 = 0;
             uint32_t cph = 0;
             while (si.next(tile, s0, s1)) {
@@ -367,7 +382,8 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                     const int nk = (2 * sg + 1 < p.KT) ? 2 : 1;
                     if (lane == 0) QOQ_TRACE_IT(p, it, 4);
                     mbar_wait(&afull[as], aph);
-                    mbar_wait(&xfull[xs], xph);
+                    if constexpr (CG == 1) mbar_wait(&xfull[xs], xph);   // CG = 2: the dequant warps of
+                    // BOTH CTAs wait on their own xfull before arriving on the leader's afull
                     if (lane == 0) QOQ_TRACE_IT(p, it, 5);
                     tc_fence_after();
                     const uint32_t a = tmem + as * 64;
@@ -376,19 +392,29 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                         for (int t = 0; t < nk; ++t) {
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
-                                mma_i8_ts(d, a + t * 32 + kk * 8, smem_desc_sw128(sb + t * C::kActBytes + kk * 32), idesc,
-                                          (local > first || t > 0 || kk > 0) ? 1u : 0u);
+                                const uint64_t bdesc = smem_desc_sw128(sb + t * C::kActBytes + kk * 32);
+                                const uint32_t accum = (local > first || t > 0 || kk > 0) ? 1u : 0u;
+                                if constexpr (CG == 2) mma_i8_ts2(d, a + t * 32 + kk * 8, bdesc, idesc, accum);
+                                else mma_i8_ts(d, a + t * 32 + kk * 8, bdesc, idesc, accum);
                                 if (p.trace && blockIdx.x == 0 && it < 16)
                                     p.trace[148 * 16 + 64 * 8 + it * 8 + t * 4 + kk] = clock64();
                             }
                         }
-                        tc_commit(&aempty[as]);      // expanded weight buffer consumed
-                        tc_commit(&xempty[xs]);      // activation slot consumed
+                        if constexpr (CG == 2) {     // free the buffers in both CTAs of the pair
+                            tc_commit2_mc(&aempty[as]);
+                            tc_commit2_mc(&xempty[xs]);
+                        } else {
+                            tc_commit(&aempty[as]);      // expanded weight buffer consumed
+                            tc_commit(&xempty[xs]);      // activation slot consumed
+                        }
                     }
                     __syncwarp();
                     if (lane == 0) QOQ_TRACE_IT(p, it, 6);
                 }
-                if (elect_one()) tc_commit(&accfull[cst]);   // this issuer's accumulator is final
+                if (elect_one()) {                              // this issuer's accumulator is final
+                    if constexpr (CG == 2) tc_commit2_mc(&accfull[cst]);
+                    else tc_commit(&accfull[cst]);
+                }
                 __syncwarp();
                 if (!si.more()) pdl_launch_dependents();      // mainloop issued: let the next kernel launch
                 if (j == 0 && lane == 0) QOQ_TRACE(p, 5);
@@ -406,7 +432,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const bool signed_a = (p.tx == nullptr);   // no t_x: feed s8 lanes (XOR), else biased u8
         const bool tw = (warp == 2 && lane == 0);
-        SegIter si(p);
+        SegIter si(p, CG);
         int tile, s0, s1, ws = 0, it = 0;
         uint32_t wph = 0;
         while (si.next(tile, s0, s1)) {
@@ -434,6 +460,10 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                     const int as = it % C::kAStages;
                     const uint32_t aph = (uint32_t)(it / C::kAStages) & 1u;
                     mbar_wait(&aempty[as], aph ^ 1);             // TMEM buffer free again
+                    if constexpr (CG == 2) {                     // this CTA's activation half landed
+                        const int xs = it % C::kXStages;
+                        mbar_wait(&xfull[xs], (uint32_t)(it / C::kXStages) & 1u);
+                    }
                     if (tw) QOQ_TRACE_IT(p, it, 2);
                     tc_fence_after();
 #pragma unroll
@@ -442,18 +472,19 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                             uint32_t out[32];
                             if (signed_a) expand_row<true>(v[t], sc[t], bias[t], out);
                             else expand_row<false>(v[t], sc[t], bias[t], out);
-                            if (tw && p.trace && blockIdx.x == 0 && it < 16)
-                                p.trace[148 * 16 + 64 * 8 + 16 * 8 + it * 8 + 2 * t] = clock64();
                             tmem_st_32x32b_x32(tmem + lane_off + as * 64 + t * 32, out);
-                            if (tw && p.trace && blockIdx.x == 0 && it < 16)
-                                p.trace[148 * 16 + 64 * 8 + 16 * 8 + it * 8 + 2 * t + 1] = clock64();
                         }
                     }
                     tmem_wait_st();
                     if (tw) QOQ_TRACE_IT(p, it, 3);
+                    if (lane == 0 && p.trace && blockIdx.x == 0 && it < 16)   // per-warp completion
+                        p.trace[148 * 16 + 64 * 8 + 16 * 8 + it * 8 + (warp - 2)] = clock64();
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&afull[as]);
+                    if (lane == 0) {
+                        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&afull[as]), 0));
+                        else mbar_arrive(&afull[as]);
+                    }
                 }
                 if (++ws == C::kWStages) { ws = 0; wph ^= 1; }
             }
@@ -466,11 +497,12 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
         const int g = et >> 5, l = et & 31;           // vector mapping: rows 4l..4l+3, tokens g, g+4, ...
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         pdl_wait();
-        SegIter si(p);
+        SegIter si(p, CG);
         int tile, s0, s1, cst = 0, it0e = 0;
         uint32_t cph = 0;
         while (si.next(tile, s0, s1)) {
-            const int nt = tile / p.MT, mt = tile % p.MT;
+            const int nt = (tile / p.MT) * CG + rank, mt = tile % p.MT;
+            tile = nt * p.MT + mt;   // the real 128-row tile of this CTA (workspace / counters index)
             const int n0 = nt * 128, m0 = mt * BN;
             // a 1-step segment lives in the accumulator of the issuer that owns that global step
             const int single = (C::kIssuers == 2 && s1 - s0 == 1) ? (it0e % 2) : 0;
@@ -559,7 +591,10 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                 if (ci == BN / C::kChunk - 1) {          // accumulators fully read: hand TMEM back
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&accempty[cst]);
+                    if (lane == 0) {
+                        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&accempty[cst]), 0));
+                        else mbar_arrive(&accempty[cst]);
+                    }
                 }
                 if (et == 0) bulk_wait_read<1>();        // staging buffer (ci & 1) no longer read by TMA
                 named_bar_sync(1, 128);
@@ -625,12 +660,14 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
     __syncthreads();
     // mode 2: no CTA may exit while its partial is still being read by a bulk reduce (completion is
     // only signalled at the leader), so the leader releases the cluster after red_full completed.
-    if (clustered) cluster_sync_all();
+    // CG = 2: the leader's MMAs read the peer's TMEM; both CTAs are past their epilogues here
+    if (clustered || CG == 2) cluster_sync_all();
     if (threadIdx.x == 0) QOQ_TRACE(p, 10);
     pdl_launch_dependents();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, C::kTmemCols);
+        if constexpr (CG == 2) tmem_dealloc2(tmem, C::kTmemCols);
+        else tmem_dealloc(tmem, C::kTmemCols);
     }
 }
 
@@ -654,12 +691,12 @@ static int max_clusters(int S) {
     static int cache[9] = {0};
     if (S < 1 || S > 8) return 0;
     if (cache[S] == 0) {
-        auto kern = w4a8_gemm_kernel<BN, false>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmemBytes);
+        auto kern = w4a8_gemm_kernel<BN, false, 1>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, 1>::kSmemBytes);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(S * 64);
         cfg.blockDim = dim3(kBlockThreads);
-        cfg.dynamicSmemBytes = Cfg<BN>::kSmemBytes;
+        cfg.dynamicSmemBytes = Cfg<BN, 1>::kSmemBytes;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = S;
@@ -732,19 +769,35 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     } else if (want == 1) {
         p.mode = 1;
         p.G = (int)(p.I < num_sms ? p.I : num_sms);
-        p.ws_bytes = (size_t)p.T * 128 * p.BN * 4 + (size_t)p.T * 4;
+        p.ws_bytes = (size_t)p.MT * p.NT * 128 * p.BN * 4 + (size_t)p.MT * p.NT * 4;
     } else {
         p.mode = 0;
         p.G = p.T < num_sms ? p.T : num_sms;
         p.ws_bytes = 0;
     }
+    // CTA pairs (cta_group::2) for modes 0 / 1 when the 128-row tiles pair up. Work units become
+    // tile pairs: T = units, G = pairs (the grid is 2G CTAs in clusters of 2).
+    const char* fp = getenv("QOQ_FORCE_CG");
+    const int force_cg = fp ? atoi(fp) : -1;
+    const bool pair_ok = p.mode != 2 && p.NT % 2 == 0 && p.BN >= 32;
+    // Opt-in for now (QOQ_FORCE_CG=2): bit-exact, but on B200 two of the four dequant warps' tcgen05.st
+    // stall for thousands of cycles while the pair's cta_group::2 MMAs run (tools/trace_gemm.py), so
+    // the pair pipeline is slower than single CTAs at decode sizes. See DESIGN.md §6.
+    p.CG = (pair_ok && force_cg == 2) ? 2 : 1;
+    if (p.CG == 2) {
+        p.T = p.MT * (p.NT / 2);
+        p.I = (long long)p.T * p.KS;
+        const int pairs = num_sms / 2;
+        if (p.mode == 0) p.G = p.T < pairs ? p.T : pairs;
+        else p.G = (int)(p.I < pairs ? p.I : pairs);
+    }
     return p;
 }
 
-template <int BN, bool OUT_I32>
+template <int BN, bool OUT_I32, int CG>
 static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t st, bool pdl) {
-    using C = Cfg<BN>;
-    auto kern = w4a8_gemm_kernel<BN, OUT_I32>;
+    using C = Cfg<BN, CG>;
+    auto kern = w4a8_gemm_kernel<BN, OUT_I32, CG>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     auto enc = encode_fn();
@@ -752,7 +805,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     CUtensorMap tm;
     cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.M};
     cuuint64_t strides[1] = {(cuuint64_t)a.K};
-    cuuint32_t box[2] = {128u, (cuuint32_t)BN};
+    cuuint32_t box[2] = {128u, (cuuint32_t)(BN / CG)};
     cuuint32_t estr[2] = {1u, 1u};
     CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a.qx), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -766,7 +819,8 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     kp.out = a.out;
     kp.ldo = a.ldo;
     kp.ws = static_cast<int32_t*>(a.ws);
-    kp.counters = a.ws ? reinterpret_cast<int*>(static_cast<uint8_t*>(a.ws) + (size_t)pl.T * 128 * BN * 4) : nullptr;
+    kp.counters = a.ws ? reinterpret_cast<int*>(static_cast<uint8_t*>(a.ws) + (size_t)pl.MT * pl.NT * 128 * BN * 4)
+                       : nullptr;
     kp.M = a.M;
     kp.MT = pl.MT;
     kp.KT = pl.KT;
@@ -778,7 +832,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     kp.I = pl.I;
     kp.trace = static_cast<unsigned long long*>(a.trace);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(pl.G);
+    cfg.gridDim = dim3(pl.G * CG);
     cfg.blockDim = dim3(kBlockThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = st;
@@ -789,9 +843,9 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
     }
-    if (pl.mode == 2) {
+    if (pl.mode == 2 || CG == 2) {
         attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = pl.S;
+        attr[na].val.clusterDim.x = CG == 2 ? 2 : pl.S;
         attr[na].val.clusterDim.y = 1;
         attr[na].val.clusterDim.z = 1;
         ++na;
@@ -801,13 +855,23 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     return cudaLaunchKernelEx(&cfg, kern, tm, kp);
 }
 
+template <int BN>
+static cudaError_t launch_bn_cg(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl) {
+    if (p.CG == 2) {
+        if constexpr (BN >= 32)
+            return a.out_i32 ? launch_bn<BN, true, 2>(a, p, st, pdl) : launch_bn<BN, false, 2>(a, p, st, pdl);
+        return cudaErrorInvalidValue;
+    }
+    return a.out_i32 ? launch_bn<BN, true, 1>(a, p, st, pdl) : launch_bn<BN, false, 1>(a, p, st, pdl);
+}
+
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl) {
     switch (p.BN) {
-        case 16: return a.out_i32 ? launch_bn<16, true>(a, p, st, pdl) : launch_bn<16, false>(a, p, st, pdl);
-        case 32: return a.out_i32 ? launch_bn<32, true>(a, p, st, pdl) : launch_bn<32, false>(a, p, st, pdl);
-        case 64: return a.out_i32 ? launch_bn<64, true>(a, p, st, pdl) : launch_bn<64, false>(a, p, st, pdl);
-        case 128: return a.out_i32 ? launch_bn<128, true>(a, p, st, pdl) : launch_bn<128, false>(a, p, st, pdl);
-        case 256: return a.out_i32 ? launch_bn<256, true>(a, p, st, pdl) : launch_bn<256, false>(a, p, st, pdl);
+        case 16: return launch_bn_cg<16>(a, p, st, pdl);
+        case 32: return launch_bn_cg<32>(a, p, st, pdl);
+        case 64: return launch_bn_cg<64>(a, p, st, pdl);
+        case 128: return launch_bn_cg<128>(a, p, st, pdl);
+        case 256: return launch_bn_cg<256>(a, p, st, pdl);
         default: return cudaErrorInvalidValue;
     }
 }

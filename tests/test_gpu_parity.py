@@ -231,3 +231,22 @@ def test_gemm_segment_edge_cases_bit_exact(gpu_lib, monkeypatch, mode, M, N, K):
         acc_ref = oracle.acc_from_packed(qx_ref, p_ref, N, K)
         a = acc.cpu().numpy()
         assert np.array_equal(a, acc_ref), f"{(a != acc_ref).sum()} accumulators differ (tx={use_tx})"
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+@pytest.mark.parametrize("M,N,K", [(64, 256, 256), (33, 1280, 1024), (64, 4096, 4096), (100, 512, 1664),
+                                   (256, 1024, 384), (40, 2560, 3200)])
+def test_gemm_cta_pair_bit_exact(gpu_lib, monkeypatch, mode, M, N, K):
+    """CTA-pair (cluster of 2, tcgen05 cta_group::2, M = 256) variant of the GEMM: the pair's
+    accumulators equal the oracle's exactly in both decompositions it supports."""
+    monkeypatch.setenv("QOQ_FORCE_MODE", mode)
+    monkeypatch.setenv("QOQ_FORCE_CG", "2")
+    W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=M * 3 + K)
+    ws = gpu_lib.Workspace(dev())
+    for use_tx in (True, False):
+        acc = gpu_lib.w4a8_gemm_i32(to_dev(qx_ref), to_dev(tx_ref) if use_tx else None, to_dev(p_ref), N,
+                                    workspace=ws)
+        assert np.array_equal(acc.cpu().numpy(), oracle.acc_from_packed(qx_ref, p_ref, N, K))
+    Y = gpu_lib.w4a8_gemm(to_dev(qx_ref), to_dev(sx_ref), to_dev(tx_ref), to_dev(p_ref), to_dev(s0_ref), N,
+                          workspace=ws)
+    check_y(Y, oracle.epilogue_f64(oracle.acc_from_packed(qx_ref, p_ref, N, K), sx_ref, s0_ref))

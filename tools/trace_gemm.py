@@ -81,11 +81,13 @@ def main():
     for i in range(16):
         if its[i, 5] > 0 and mm[i, 0] > 0:
             print(f"   it{i:2d} " + " ".join(f"{int(v - its[i, 5]):6d}" for v in mm[i] if v > 0))
-    print("  CTA 0 dequant detail (cycles after xready): comp0 st0_issued comp1 st1_issued | wait_st_done")
+    print("  CTA 0 per-warp dequant completion (cycles after the traced warp's xready) | mma_go - slowest")
     for i in range(16):
-        if its[i, 2] > 0 and dq[i, 0] > 0:
-            print(f"   it{i:2d} " + " ".join(f"{int(v - its[i, 2]):6d}" for v in dq[i, :4] if v > 0)
-                  + f" | {int(its[i, 3] - its[i, 2]):6d}")
+        if its[i, 2] > 0:
+            done = [v for v in dq[i] if v > 0]
+            if done:
+                print(f"   it{i:2d} " + " ".join(f"{int(v - its[i, 2]):6d}" for v in done)
+                      + f" | {int(its[i, 5] - max(done)):6d}")
 
 
 if __name__ == "__main__":
