@@ -41,17 +41,21 @@
 namespace qoq {
 
 #ifndef QOQ_DEQ_GROUPS
-#define QOQ_DEQ_GROUPS 2
+#define QOQ_DEQ_GROUPS 3
 #endif
-constexpr int kDeqGroups = QOQ_DEQ_GROUPS;   // 4-warp dequant groups taking steps round-robin
-constexpr int kDeqWarp1 = 2 + 4 * kDeqGroups;        // first warp after the dequant warps
-constexpr int kEpiWarp0 = kDeqWarp1;                 // epilogue: 4 warps
-constexpr int kMma1Warp = kEpiWarp0 + 4;             // MMA issuer 1
-constexpr int kXProdWarp = kMma1Warp + 1;            // activation producer
-constexpr int kBlockThreads = 32 * (kXProdWarp + 1);
-constexpr int kThreads = 448;       // + 64 below: warps 0 weight producer, 1 MMA issuer 0 + TMEM owner,
-                                    // 2-9 dequant, 10-13 epilogue, 14 MMA issuer 1, 15 activation producer
-constexpr int kEpiThread0 = 32 * kEpiWarp0;   // first epilogue thread
+
+// Warp roles (per Cfg): 0 weight producer, 1 MMA issuer 0 + TMEM owner, 2 .. 2+4G-1 dequant (G groups
+// of 4 warps taking steps round-robin), then 4 epilogue warps, MMA issuer 1, activation producer.
+template <int G>
+struct Roles {
+    static constexpr int kDeqGroups = G;
+    static constexpr int kDeqWarp1 = 2 + 4 * G;          // first warp after the dequant warps
+    static constexpr int kEpiWarp0 = kDeqWarp1;          // epilogue: 4 warps
+    static constexpr int kMma1Warp = kEpiWarp0 + 4;      // MMA issuer 1
+    static constexpr int kXProdWarp = kMma1Warp + 1;     // activation producer
+    static constexpr int kBlockThreads = 32 * (kXProdWarp + 1);
+    static constexpr int kEpiThread0 = 32 * kEpiWarp0;   // first epilogue thread
+};
 
 // One pipeline STEP = up to two consecutive 128-deep k-tiles of one output tile: the handoff
 // (dequant -> MMA, MMA -> producer) is amortized over 8 MMAs, and two MMA-issuing warps take
@@ -65,6 +69,11 @@ constexpr int kEpiThread0 = 32 * kEpiWarp0;   // first epilogue thread
 // 32 cycles per 256x64x32 MMA vs 45.5 per 128x64x32 on one SM).
 template <int BN, int CG = 1>
 struct Cfg {
+    // dequant groups: QOQ_DEQ_GROUPS (default 3; measured +1..9% over 2 at decode) where the TMEM budget allows a rotation-compatible
+    // A ring, else 2
+    static constexpr int kDeqGroups = (BN <= 64) ? QOQ_DEQ_GROUPS : 2;
+    using R = Roles<kDeqGroups>;
+    static constexpr int kBlockThreads = R::kBlockThreads;
     static constexpr int kIssuers = BN <= 128 ? 2 : 1;
     static constexpr int kActRows = BN / CG;                          // activation rows held by this CTA
     static constexpr int kActBytes = kActRows * 128;                  // one k-tile of this CTA's activations
@@ -72,11 +81,10 @@ struct Cfg {
     static constexpr int kChunk = BN < 32 ? BN : 32;                  // TMEM columns per epilogue tcgen05.ld
     static constexpr int kStgBytes = kChunk * 128 * 4;                // one INT32 staging buffer [kChunk][128]
     static constexpr int kEpiBytes = 2 * kStgBytes + BN * 8;          // 2 staging buffers + per-token s_x, 128 t_x
-#ifndef QOQ_ACC_STAGES
-    static constexpr int kAccStages = (2 * kIssuers * BN + 4 * 64 <= 512) ? 2 : 1;
-#else
-    static constexpr int kAccStages = (QOQ_ACC_STAGES * kIssuers * BN + 4 * 64 <= 512) ? QOQ_ACC_STAGES : 1;
-#endif
+    static constexpr int kARot = kDeqGroups % 2 == 0 ? kDeqGroups : 2 * kDeqGroups;   // lcm(2, groups)
+    // two accumulator stages if they leave room for at least one A-ring rotation (2 x 64 columns
+    // per rotation unit), else one
+    static constexpr int kAccStages = ((512 - 2 * kIssuers * BN) / 64 >= (kARot > 4 ? kARot : 4)) ? 2 : 1;
     static constexpr int kAccCols = kAccStages * kIssuers * BN;
     // Three independent rings: W (packed weights, HBM-latency bound, SMEM), X (activation k-tiles,
     // L2-latency bound, SMEM) and A (expanded weights, 64 TMEM columns per step). (Loading weights
@@ -85,12 +93,11 @@ struct Cfg {
     // Ring depths are multiples of the number of roles that take turns on them (dequant groups on
     // W and A, the two MMA issuers on A and X), so every slot is always consumed by the same role
     // and no waiter can run two mbarrier phases ahead (parity waits would alias).
-    static constexpr int kARot = kDeqGroups % 2 == 0 ? kDeqGroups : 2 * kDeqGroups;   // lcm(2, groups)
     static constexpr int kARaw0 = (512 - kAccCols) / 64;
     static constexpr int kARaw = kARaw0 > 6 ? 6 : kARaw0;
     static constexpr int kAStages = (kARaw / kARot) * kARot;
 #ifndef QOQ_XSTAGES
-    static constexpr int kXStages = BN <= 32 ? 8 : BN == 64 ? 6 : 2;
+    static constexpr int kXStages = BN <= 32 ? (kDeqGroups == 3 ? 6 : 8) : BN == 64 ? 6 : 2;
 #else
     static constexpr int kXStages = BN <= 64 ? QOQ_XSTAGES : 2;
 #endif
@@ -110,6 +117,7 @@ struct Cfg {
     static constexpr int kFinU = BN / 4 < 8 ? BN / 4 : 8;             // independent 16-B loads per finalize batch
     static_assert(kXStages >= 2 && kWStages >= 2 && kAStages >= 2, "pipeline too shallow");
     static_assert(kXStages % kIssuers == 0 && kWStages % kDeqGroups == 0 && kAStages % kARot == 0, "ring rotation");
+    static_assert(CG == 1 || kXStages % kDeqGroups == 0, "ring rotation (pairs: dequant groups wait on X)");
     static_assert(kColsUsed <= 512, "TMEM overflow");
     static_assert(kSmemBytes <= 227 * 1024, "SMEM overflow");
 };
@@ -226,7 +234,7 @@ __device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<
 }
 
 template <int BN, bool OUT_I32, int CG>
-__global__ void __launch_bounds__(kBlockThreads, 1)
+__global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
     using C = Cfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
@@ -330,7 +338,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                 }
             }
         }
-    } else if (warp == kXProdWarp) {
+    } else if (warp == C::R::kXProdWarp) {
         // ===================== activation producer: TMA 2-D (SWIZZLE_128B) k-tiles of q_x
         if (lane == 0) {
             pdl_wait();
@@ -357,7 +365,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                 }
             }
         }
-    } else if (warp == 1 || warp == kMma1Warp) {
+    } else if (warp == 1 || warp == C::R::kMma1Warp) {
         // ===================== MMA issuers (one thread each). Issuer j takes the steps of a segment
         // with local index % kIssuers == j, accumulating into its own TMEM accumulator. It waits only
         // on afull[x]: the dequant warps arrive there after acquiring xfull[x], so the TMA-written
@@ -422,7 +430,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                 if (++cst == C::kAccStages) { cst = 0; cph ^= 1; }
             }
         }
-    } else if (warp >= 2 && warp < kDeqWarp1) {
+    } else if (warp >= 2 && warp < C::R::kDeqWarp1) {
         // ===================== dequant: u4 -> (q̂ + 128) lanes -> TMEM buffer of the step's X slot
         // Two 4-warp groups take alternate steps; in a group, warp (w & 3) owns TMEM lanes
         // 32(w&3)..+31 and thread r expands weight row r of each k-tile (32 TMEM columns per tile).
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
         uint32_t wph = 0;
         while (si.next(tile, s0, s1)) {
             for (int sg = s0; sg < s1; ++sg, ++it) {
-                if (it % kDeqGroups == grp) {
+                if (it % C::kDeqGroups == grp) {
                     const int nk = (2 * sg + 1 < p.KT) ? 2 : 1;
                     mbar_wait(&wfull[ws], wph);
                     if (tw) QOQ_TRACE_IT(p, it, 0);
@@ -489,11 +497,11 @@ __global__ void __launch_bounds__(kBlockThreads, 1)
                 if (++ws == C::kWStages) { ws = 0; wph ^= 1; }
             }
         }
-    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+    } else if (warp >= C::R::kEpiWarp0 && warp < C::R::kEpiWarp0 + 4) {
         // ===================== epilogue (warps 10-13)
         const int q = warp & 3;
         const int r = q * 32 + lane;                  // TMEM lane = weight row within the tile
-        const int et = threadIdx.x - kEpiThread0;     // 0..127 for cooperative phases
+        const int et = threadIdx.x - C::R::kEpiThread0;   // 0..127 for cooperative phases
         const int g = et >> 5, l = et & 31;           // vector mapping: rows 4l..4l+3, tokens g, g+4, ...
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         pdl_wait();
@@ -695,7 +703,7 @@ static int max_clusters(int S) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, 1>::kSmemBytes);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(S * 64);
-        cfg.blockDim = dim3(kBlockThreads);
+        cfg.blockDim = dim3(Cfg<BN, 1>::kBlockThreads);
         cfg.dynamicSmemBytes = Cfg<BN, 1>::kSmemBytes;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -833,7 +841,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     kp.trace = static_cast<unsigned long long*>(a.trace);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.G * CG);
-    cfg.blockDim = dim3(kBlockThreads);
+    cfg.blockDim = dim3(C::kBlockThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
