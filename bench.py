@@ -232,6 +232,9 @@ def config_dict(args, world):
                         f"M={args.M} tokens, W4A8 g128, per-token INT8 activations",
             "model_shapes": args.model, "M": args.M, "layers": layers, "group": 128,
             "parallelism": f"tp{world}" if world > 1 else "single",
+            "activation_quant": ("fused into the GEMM prologue (qoq_w4a8_linear)"
+                                 if getattr(args, "fused_quant", False) and args.M <= 64
+                                 else "separate kernel (quantizer + GEMM, PDL-chained)"),
             "l2": "weights stream from HBM: packed stack >> 126 MB L2 (no flush needed)"}
 
 
@@ -252,6 +255,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="per-projection GEMM breakdown and M sweep")
     ap.add_argument("--unfused-gate-up", action="store_true", help="run gate and up as two GEMMs")
+    ap.add_argument("--fused-quant", action="store_true",
+                    help="qoq_w4a8_linear per linear: per-token quantization fused into the GEMM prologue "
+                         "(M <= 64); default: quantizer kernel + GEMM, chained with PDL (faster today)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -300,14 +306,25 @@ def main():
     quant_out = {qg: (torch.empty(M, K, dtype=torch.int8, device=dev), torch.empty(M, dtype=torch.float16, device=dev),
                       torch.empty(M, dtype=torch.int32, device=dev)) for qg, K in Kin.items()}
     Ybuf = {name: torch.empty(M, N, dtype=torch.float16, device=dev) for name, N, K, kind, qg in shapes}
-    ws = qoq.Workspace(dev)
+    ws = qoq.Workspace(dev)      # GEMM workspace (kept all-zero by the library)
     ws.get(max(qoq.gemm_workspace_bytes(M, N, K) for _, N, K, _, _ in shapes))
+    lws = qoq.Workspace(dev)     # linear workspace (also holds the call's q_x / s_x / t_x)
+    lws.get(max(qoq.linear_workspace_bytes(M, N, K) for _, N, K, _, _ in shapes))
+    fused_quant = args.fused_quant
 
     def run_step(gemm_only=False):
         n_launch = 0
         for l in range(layers):
             done = set()
             for i, (name, N, K, kind, qg) in enumerate(shapes):
+                if fused_quant and not gemm_only:
+                    # the public linear call: per-token quantization fused into the GEMM (M <= 64)
+                    p, s0 = packed[l][i]
+                    qoq.w4a8_linear(X[qg], p, s0, N, out=Ybuf[name], workspace=lws, stream=stream)
+                    n_launch += qoq.linear_launches(M)
+                    if kind == "row" and world > 1:
+                        dist.all_reduce(Ybuf[name])
+                    continue
                 if not gemm_only and qg not in done:
                     qoq.quantize_activations_per_token(X[qg], out=quant_out[qg], stream=stream)
                     done.add(qg)
@@ -365,15 +382,24 @@ def main():
     step_bytes, step_ops = step_work(args.model, M, layers, world, fused)
     value = step_bytes / (ms_step * 1e-3) / 1e9
 
-    # dominant kernel: the W4A8 GEMM (per-rank launches in the gemm-only graph)
-    rank_gemm_bytes = sum(gemm_bytes(M, N, K) for _, N, K, _, _ in shapes) * layers
-    per_launch_ms = ms_gemm / max(10, args.steps // 2) / gemm_launches
-    per_launch_bytes = rank_gemm_bytes / gemm_launches
+    # dominant kernel: the W4A8 GEMM. Fused (default, M <= 64): every launch of the step is the GEMM
+    # kernel with the quantization in its prologue, so its per-launch figures come from the step;
+    # two-kernel: the GEMM-only graph.
+    if fused_quant and qoq.linear_launches(M) == 1:
+        rank_gemm_bytes = sum(gemm_bytes(M, N, K) + quant_bytes(M, K) for _, N, K, _, _ in shapes) * layers
+        per_launch_ms = ms_step / launches_per_step
+        per_launch_bytes = rank_gemm_bytes / launches_per_step
+        kernel_name = "w4a8_gemm_kernel (per-token quantization fused)"
+    else:
+        rank_gemm_bytes = sum(gemm_bytes(M, N, K) for _, N, K, _, _ in shapes) * layers
+        per_launch_ms = ms_gemm / max(10, args.steps // 2) / gemm_launches
+        per_launch_bytes = rank_gemm_bytes / gemm_launches
+        kernel_name = "w4a8_gemm_kernel"
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
     peak, peak_src = load_peaks()
-    traffic = load_traffic(f"{args.model}-M{M}")
+    traffic = load_traffic(f"{args.model}-M{M}" + ("-fused" if kernel_name != "w4a8_gemm_kernel" else ""))
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "w4a8_gemm_kernel",
+                "traffic": traffic, "kernel": kernel_name,
                 "algorithmic_bytes_per_launch": per_launch_bytes, "avg_launch_us": per_launch_ms * 1e3,
                 "peak_source": peak_src}
     tops = step_ops / (ms_step * 1e-3) / 1e12

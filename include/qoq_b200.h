@@ -40,7 +40,7 @@ typedef enum {
 const char* qoq_status_string(int status);
 /* ABI version of this header (incremented on any signature or layout change). */
 int qoq_abi_version(void);
-#define QOQ_ABI_VERSION 1
+#define QOQ_ABI_VERSION 2
 
 /* ----------------------------------------------------------------------------------------------
  * Packed weight layout (frozen). The B200 form of "store the weights in the order
@@ -103,9 +103,29 @@ int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed,
                       int32_t* acc, int ldacc,
                       void* workspace, size_t workspace_bytes, void* stream);
 
+/* The W4A8 linear layer on fp16 activations: per-token INT8 quantization of X (exactly
+ * qoq_quantize_activations_per_token) followed by the W4A8 GEMM (exactly qoq_w4a8_gemm), so
+ *   Y = qoq_w4a8_gemm(quantize(X))  bit for bit.
+ * For M <= 64 (decode) both run in ONE kernel: the GEMM's epilogue warps quantize rows
+ * m ≡ cta (mod grid) into the workspace while the weight stream is already in flight, and a grid
+ * handshake in the workspace releases the activation loads; above 64 it launches the quantizer
+ * kernel and then the GEMM.
+ *   X_fp16 [M][ldx] (ldx >= K, ldx % 8 == 0, 16-byte aligned).  packed / s0_fp16 from
+ *   qoq_quantize_weights.  Y_fp16 [M][ldy], ldy >= N, ldy % 4 == 0.
+ * workspace: qoq_linear_workspace_bytes(M,N,K) bytes, 256-byte aligned, ZERO-FILLED before first
+ * use; each call leaves its synchronization words and split-K partials zeroed again. Layout, each
+ * part 256-byte aligned: [256 B sync][q_x int8 M*K][s_x fp16 M][t_x int32 M][GEMM workspace];
+ * after the call q_x / s_x / t_x hold this call's quantized activations. One workspace per stream.
+ * Same shape requirements as qoq_w4a8_gemm. */
+size_t qoq_linear_workspace_bytes(int M, int N, int K);
+int qoq_w4a8_linear(const void* X_fp16, int ldx, int M, int N, int K, int group,
+                    const void* packed, const void* s0_fp16,
+                    void* Y_fp16, int ldy,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
 /* End-to-end linear layer with HOST activations (the e2e measurement path): copies X_host
- * (pinned host memory, [M][K] fp16) to the device, quantizes it per token, runs the W4A8 GEMM
- * against device-resident packed weights and copies Y back to Y_host ([M][N] fp16, pinned).
+ * (pinned host memory, [M][K] fp16) to the device, runs qoq_w4a8_linear against device-resident
+ * packed weights and copies Y back to Y_host ([M][N] fp16, pinned).
  * dev_scratch: qoq_linear_host_scratch_bytes(M,N,K) bytes of device memory, zero-filled
  * before first use (it embeds the GEMM workspace). Asynchronous on `stream`. */
 size_t qoq_linear_host_scratch_bytes(int M, int N, int K);
@@ -115,7 +135,7 @@ int qoq_linear_host(const void* X_host_fp16, int M, int K,
 
 /* Kernels launched per successful call (launch accounting for benchmarks):
  * quantize_weights 2, quantize_activations_per_token 1, w4a8_gemm 1, w4a8_gemm_i32 1,
- * linear_host 2 (plus 2 async copies). */
+ * w4a8_linear 1 (M <= 64) or 2, linear_host as w4a8_linear (plus 2 async copies). */
 
 #ifdef __cplusplus
 }

@@ -23,10 +23,16 @@ LIB_PATH = os.path.join(_HERE, "libqoq_b200.so" if not os.environ.get("QOQ_LIB_V
                         else f"libqoq_b200_{os.environ['QOQ_LIB_VARIANT']}.so")
 GROUP = 128
 TILE_BYTES = 8448
-ABI_VERSION = 1
+ABI_VERSION = 2
 # kernels launched per call (matches include/qoq_b200.h)
 LAUNCHES = {"quantize_weights": 2, "quantize_activations_per_token": 1, "w4a8_gemm": 1,
-            "w4a8_gemm_i32": 1, "linear_host": 2}
+            "w4a8_gemm_i32": 1}
+FUSE_MAX_M = 64   # w4a8_linear / linear_host: one fused kernel up to this M, quantizer + GEMM above
+
+
+def linear_launches(M: int) -> int:
+    """Kernels one w4a8_linear (or linear_host) call launches."""
+    return 1 if M <= FUSE_MAX_M else 2
 
 _lock = threading.Lock()
 _lib = None
@@ -57,6 +63,8 @@ def load() -> ctypes.CDLL:
             "qoq_gemm_workspace_bytes": (Z, [I, I, I]),
             "qoq_w4a8_gemm": (I, [P, P, P, P, P, I, I, I, I, P, I, P, Z, P]),
             "qoq_w4a8_gemm_i32": (I, [P, P, P, I, I, I, I, P, I, P, Z, P]),
+            "qoq_linear_workspace_bytes": (Z, [I, I, I]),
+            "qoq_w4a8_linear": (I, [P, I, I, I, I, I, P, P, P, I, P, Z, P]),
             "qoq_linear_host_scratch_bytes": (Z, [I, I, I]),
             "qoq_linear_host": (I, [P, I, I, P, P, I, P, P, Z, P]),
         }
@@ -99,6 +107,23 @@ def gemm_workspace_bytes(M: int, N: int, K: int) -> int:
     return load().qoq_gemm_workspace_bytes(M, N, K)
 
 
+def linear_workspace_bytes(M: int, N: int, K: int) -> int:
+    return load().qoq_linear_workspace_bytes(M, N, K)
+
+
+def linear_workspace_views(ws: torch.Tensor, M: int, K: int):
+    """(qx [M][K] int8, sx [M] fp16, tx [M] int32) views of a qoq_w4a8_linear workspace (header layout)."""
+    def up(v):
+        return (v + 255) // 256 * 256
+    o_qx = 256
+    o_sx = o_qx + up(M * K)
+    o_tx = o_sx + up(2 * M)
+    qx = ws[o_qx:o_qx + M * K].view(torch.int8).view(M, K)
+    sx = ws[o_sx:o_sx + 2 * M].view(torch.float16)
+    tx = ws[o_tx:o_tx + 4 * M].view(torch.int32)
+    return qx, sx, tx
+
+
 def linear_host_scratch_bytes(M: int, N: int, K: int) -> int:
     return load().qoq_linear_host_scratch_bytes(M, N, K)
 
@@ -138,7 +163,9 @@ def quantize_activations_per_token(X: torch.Tensor, K: int | None = None, want_t
 
 
 class Workspace:
-    """Zero-filled GEMM workspace that grows on demand (the library leaves it zeroed)."""
+    """Zero-filled workspace that grows on demand. A GEMM workspace is left zeroed by the library; a
+    linear (w4a8_linear) workspace additionally holds the last call's q_x / s_x / t_x, so do not pass
+    the same Workspace to both kinds of call."""
 
     def __init__(self, device=None):
         self.device = device
@@ -155,9 +182,12 @@ class Workspace:
 _default_ws: dict = {}
 
 
-def _ws_for(device, nbytes, workspace):
+def _ws_for(device, nbytes, workspace, kind="gemm"):
+    """Default workspaces are per (device, stream, kind): a GEMM workspace must stay all-zero between
+    calls, while a linear workspace also holds the call's quantized activations, so the two kinds
+    never share a buffer."""
     if workspace is None:
-        key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream, kind)
         workspace = _default_ws.setdefault(key, Workspace(device))
     return workspace.get(nbytes)
 
@@ -187,16 +217,31 @@ def w4a8_gemm_i32(qx: torch.Tensor, tx: torch.Tensor | None, packed: torch.Tenso
     return acc
 
 
+def w4a8_linear(X: torch.Tensor, packed: torch.Tensor, s0: torch.Tensor, N: int, K: int | None = None,
+                out: torch.Tensor | None = None, workspace: Workspace | None = None, stream=None) -> torch.Tensor:
+    """Y [M][N] fp16 = w4a8_gemm(quantize_activations_per_token(X)) bit for bit; ONE fused kernel for
+    M <= 64 (quantization in the GEMM's prologue), quantizer + GEMM above. X [M][ldx] fp16, K <= ldx."""
+    if X.dtype != torch.float16 or X.dim() != 2:
+        raise ValueError("X must be a 2-D fp16 tensor")
+    M, ldx = X.shape
+    K = ldx if K is None else K
+    Y = torch.empty(M, N, dtype=torch.float16, device=X.device) if out is None else out
+    ws, wsb = _ws_for(X.device, linear_workspace_bytes(M, N, K), workspace, kind="linear")
+    _check("qoq_w4a8_linear",
+           load().qoq_w4a8_linear(_ptr(X), ldx, M, N, K, GROUP, _ptr(packed), _ptr(s0), _ptr(Y), Y.stride(0),
+                                  _ptr(ws), wsb, _stream(stream)))
+    return Y
+
+
 def linear(X: torch.Tensor, packed: torch.Tensor, s0: torch.Tensor, N: int, K: int | None = None,
            workspace: Workspace | None = None, stream=None) -> torch.Tensor:
-    """Quantize X per token, then W4A8 GEMM (two kernels, chained with PDL)."""
-    qx, sx, tx = quantize_activations_per_token(X, K, stream=stream)
-    return w4a8_gemm(qx, sx, tx, packed, s0, N, workspace=workspace, stream=stream)
+    """The W4A8 linear layer: per-token quantization + GEMM (w4a8_linear)."""
+    return w4a8_linear(X, packed, s0, N, K, workspace=workspace, stream=stream)
 
 
 def linear_host(X_host: torch.Tensor, packed: torch.Tensor, s0: torch.Tensor, N: int,
                 Y_host: torch.Tensor, scratch: torch.Tensor, stream=None):
-    """End-to-end through the C ABI with pinned HOST X/Y: H2D, quantize, GEMM, D2H (async)."""
+    """End-to-end through the C ABI with pinned HOST X/Y: H2D, w4a8_linear, D2H (async)."""
     if X_host.is_cuda or Y_host.is_cuda:
         raise ValueError("linear_host takes host tensors")
     M, K = X_host.shape

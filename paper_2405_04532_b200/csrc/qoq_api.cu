@@ -59,6 +59,56 @@ int run_gemm(const int8_t* qx, const void* sx, const int32_t* tx, const void* pa
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// qoq_w4a8_linear workspace: [qsync 2 x int32][q_x M*K][s_x 2M][t_x 4M][GEMM workspace], 256-B aligned
+struct LinearWs {
+    int* qsync;
+    int8_t* qx;
+    void* sx;
+    int32_t* tx;
+    void* gemm_ws;
+    size_t gemm_ws_bytes, total;
+};
+
+LinearWs linear_ws_layout(void* base, int M, int N, int K) {
+    LinearWs w{};
+    uint8_t* b = static_cast<uint8_t*>(base);
+    size_t off = 0;
+    w.qsync = reinterpret_cast<int*>(b + off);  off += 256;
+    w.qx = reinterpret_cast<int8_t*>(b + off);  off += align_up((size_t)M * K, 256);
+    w.sx = b + off;                              off += align_up((size_t)M * 2, 256);
+    w.tx = reinterpret_cast<int32_t*>(b + off); off += align_up((size_t)M * 4, 256);
+    w.gemm_ws = b + off;
+    w.gemm_ws_bytes = plan_gemm(M, N, K, num_sms_or_default()).ws_bytes;
+    w.total = off + align_up(w.gemm_ws_bytes, 256);
+    return w;
+}
+
+int run_linear(const void* X, int ldx, int M, int N, int K, int group, const void* packed, const void* s0,
+               void* Y, int ldy, void* ws, size_t ws_bytes, cudaStream_t st, void* trace = nullptr) {
+    int rc = gemm_shape_status(M, N, K, group);
+    if (rc) return rc;
+    if (ldx < K || ldx % 8 || ldy < N) return QOQ_ERR_INVALID_ARG;
+    if (M == 0) return QOQ_OK;
+    if (!X || !aligned16(X) || !packed || !s0 || !Y || !ws) return QOQ_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return QOQ_ERR_INVALID_ARG;
+    LinearWs w = linear_ws_layout(ws, M, N, K);
+    if (ws_bytes < w.total) return QOQ_ERR_WORKSPACE;
+    if (M > kFuseMaxM) {
+        if ((rc = qoq_quantize_activations_per_token(X, M, K, ldx, w.qx, w.sx, w.tx, st))) return rc;
+        return run_gemm(w.qx, w.sx, w.tx, packed, s0, M, N, K, group, Y, ldy, false, w.gemm_ws, w.gemm_ws_bytes,
+                        st);
+    }
+    if (ldy % 4 != 0 || !aligned16(Y) || !aligned16(s0) || !aligned16(packed)) return QOQ_ERR_INVALID_ARG;
+    int sms = 0;
+    if ((rc = check_arch(&sms))) return rc;
+    GemmPlan p = plan_gemm(M, N, K, sms);
+    GemmArgs a{w.qx, w.sx, w.tx, packed, s0, Y, ldy, false, M, N, K, p.ws_bytes ? w.gemm_ws : nullptr, trace};
+    a.X = X;
+    a.ldx = ldx;
+    a.qsync = w.qsync;
+    return launch_w4a8_gemm(a, p, st, /*pdl=*/true) == cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
 }  // namespace
 
 extern "C" {
@@ -127,6 +177,16 @@ int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed, i
                     static_cast<cudaStream_t>(stream));
 }
 
+size_t qoq_linear_workspace_bytes(int M, int N, int K) {
+    if (gemm_shape_status(M, N, K, 128) != QOQ_OK) return 0;
+    return linear_ws_layout(nullptr, M, N, K).total;
+}
+
+int qoq_w4a8_linear(const void* X, int ldx, int M, int N, int K, int group, const void* packed, const void* s0,
+                    void* Y, int ldy, void* ws, size_t ws_bytes, void* stream) {
+    return run_linear(X, ldx, M, N, K, group, packed, s0, Y, ldy, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
 // Debug (not in the public header): the fp16 GEMM with a per-CTA %globaltimer trace
 // (16 x u64 per CTA, grid <= #SMs) for pipeline timeline analysis (tools/trace_gemm.py).
 int qoq_debug_w4a8_gemm_trace(const int8_t* qx, const void* sx, const int32_t* tx, const void* packed,
@@ -136,12 +196,16 @@ int qoq_debug_w4a8_gemm_trace(const int8_t* qx, const void* sx, const int32_t* t
                     static_cast<cudaStream_t>(stream), trace);
 }
 
-// scratch layout: [X fp16 M*K][qx M*K][sx 2M][tx 4M][Y fp16 M*N][gemm workspace], each 256-B aligned
+// Debug (not in the public header): qoq_w4a8_linear with the same per-CTA trace.
+int qoq_debug_w4a8_linear_trace(const void* X, int M, int N, int K, const void* packed, const void* s0, void* Y,
+                                void* ws, size_t ws_bytes, void* trace, void* stream) {
+    return run_linear(X, K, M, N, K, 128, packed, s0, Y, N, ws, ws_bytes, static_cast<cudaStream_t>(stream), trace);
+}
+
+// scratch layout: [X fp16 M*K][Y fp16 M*N][linear workspace], each 256-B aligned
 size_t qoq_linear_host_scratch_bytes(int M, int N, int K) {
     if (gemm_shape_status(M, N, K, 128) != QOQ_OK) return 0;
-    size_t b = align_up((size_t)M * K * 2, 256) + align_up((size_t)M * K, 256) + align_up((size_t)M * 2, 256) +
-               align_up((size_t)M * 4, 256) + align_up((size_t)M * N * 2, 256);
-    return b + align_up(qoq_gemm_workspace_bytes(M, N, K), 256);
+    return align_up((size_t)M * K * 2, 256) + align_up((size_t)M * N * 2, 256) + qoq_linear_workspace_bytes(M, N, K);
 }
 
 int qoq_linear_host(const void* X_host, int M, int K, const void* packed, const void* s0, int N, void* Y_host,
@@ -149,21 +213,17 @@ int qoq_linear_host(const void* X_host, int M, int K, const void* packed, const 
     int rc = gemm_shape_status(M, N, K, 128);
     if (rc) return rc;
     if (M == 0) return QOQ_OK;
-    if (!X_host || !Y_host || !packed || !s0 || !scratch || !aligned16(scratch)) return QOQ_ERR_INVALID_ARG;
+    if (!X_host || !Y_host || !packed || !s0 || !scratch || (reinterpret_cast<uintptr_t>(scratch) & 255u))
+        return QOQ_ERR_INVALID_ARG;
     if (scratch_bytes < qoq_linear_host_scratch_bytes(M, N, K)) return QOQ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint8_t* b = static_cast<uint8_t*>(scratch);
     void* Xd = b;                b += align_up((size_t)M * K * 2, 256);
-    int8_t* qx = (int8_t*)b;     b += align_up((size_t)M * K, 256);
-    void* sx = b;                b += align_up((size_t)M * 2, 256);
-    int32_t* tx = (int32_t*)b;   b += align_up((size_t)M * 4, 256);
     void* Yd = b;                b += align_up((size_t)M * N * 2, 256);
     void* ws = b;
     if (cudaMemcpyAsync(Xd, X_host, (size_t)M * K * 2, cudaMemcpyHostToDevice, st) != cudaSuccess)
         return QOQ_ERR_CUDA;
-    if ((rc = qoq_quantize_activations_per_token(Xd, M, K, K, qx, sx, tx, stream))) return rc;
-    if ((rc = qoq_w4a8_gemm(qx, sx, tx, packed, s0, M, N, K, 128, Yd, N, ws, qoq_gemm_workspace_bytes(M, N, K),
-                            stream)))
+    if ((rc = run_linear(Xd, K, M, N, K, 128, packed, s0, Yd, N, ws, qoq_linear_workspace_bytes(M, N, K), st)))
         return rc;
     if (cudaMemcpyAsync(Y_host, Yd, (size_t)M * N * 2, cudaMemcpyDeviceToHost, st) != cudaSuccess)
         return QOQ_ERR_CUDA;

@@ -40,7 +40,14 @@ struct GemmArgs {
     int M, N, K;
     void* ws;
     void* trace = nullptr;   // debug timeline buffer (16 u64 per CTA) or nullptr
+    // fused per-token quantization (M <= kFuseMaxM): X [M][ldx] fp16 is quantized inside the GEMM
+    // into qx / sx / tx (then outputs, not inputs); qsync: 2 zero-initialized ints
+    const void* X = nullptr;
+    int ldx = 0;
+    int* qsync = nullptr;
 };
+
+constexpr int kFuseMaxM = 64;   // above: quantizer kernel + GEMM (the prologue would serialize M rows)
 
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl);
 cudaError_t launch_quantize_weights(const void* W, int N, int K, void* packed, void* s0, cudaStream_t st);

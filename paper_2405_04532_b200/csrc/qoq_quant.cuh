@@ -1,0 +1,96 @@
+// qoq_quant.cuh — device helpers of the per-token symmetric INT8 activation quantization
+// (P:813), shared by the standalone quantizer (quantize.cu) and the fused prologue of the
+// W4A8 GEMM (w4a8_gemm.cu), so both produce bit-identical q_x / s_x / t_x.
+// Floating-point decisions: IEEE fp32 division (__fdiv_rn, no fast-math), round-half-away (roundf),
+// __float2half_rn (DESIGN.md §3 readings).
+#pragma once
+#include <cuda_fp16.h>
+#include <cstdint>
+
+namespace qoq {
+
+// Symmetric fp16 scale: fp16_rn(amax / qmax); 1.0 for amax == 0; 2^-24 if it underflows to 0.
+__device__ __forceinline__ __half sym_scale(float amax, float qmax) {
+    if (amax == 0.0f) return __float2half_rn(1.0f);
+    __half s = __float2half_rn(__fdiv_rn(amax, qmax));
+    if ((__half_as_ushort(s) & 0x7fff) == 0) s = __ushort_as_half(1);
+    return s;
+}
+
+__device__ __forceinline__ float amax8(uint4 v, float a) {
+    const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 f = __half22float2(h[i]);
+        a = fmaxf(a, fmaxf(fabsf(f.x), fabsf(f.y)));
+    }
+    return a;
+}
+
+// max |x| over 8 fp16 in half2 arithmetic (exact: |x| and max are exact in fp16; finite inputs)
+__device__ __forceinline__ __half2 amax8h(uint4 v, __half2 a) {
+    const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a = __hmax2(a, __habs2(h[i]));
+    return a;
+}
+__device__ __forceinline__ float amax_of(__half2 a) {
+    return fmaxf(__low2float(a), __high2float(a));
+}
+
+
+
+// q = clamp(round_half_away(fl32(x / s)), ±127), the oracle's definition, by the division (exact
+// path, taken rarely — see quant8).
+__device__ __forceinline__ int quant_code_exact(float x, float s) {
+    return min(127, max(-127, (int)roundf(__fdiv_rn(x, s))));
+}
+
+static __device__ __noinline__ uint2 quant8_exact(uint4 u, float s, int& t) {
+    const __half* h = reinterpret_cast<const __half*>(&u);
+    uint32_t w[2] = {0, 0};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int q = quant_code_exact(__half2float(h[e]), s);
+        t += q;
+        w[e >> 2] |= (uint32_t)(q & 0xff) << (8 * (e & 3));
+    }
+    return make_uint2(w[0], w[1]);
+}
+
+// 8 fp16 -> 8 int8 codes clamp(⌈x / s⌋, ±127), bit-identical to quant_code_exact, accumulating their
+// sum into t (inv = __frcp_rn(s)). Without a division: r = fl(x * inv) is within
+// (2^-24 + 2^-24 + 2^-48)|x/s| of x/s and fl(x/s) within 2^-24 |x/s|, so for |x/s| < 128 the two
+// differ by < 2^-15. Unless r lies within 2^-14 of a half-integer, both therefore round to the same
+// integer, and away from ties round-half-away equals round-to-nearest (rintf). Clamping r to ±127
+// first is exact too (r >= 127 implies fl(x/s) > 126.99, which rounds and clamps to 127). Only if
+// one of the 8 is near a tie (probability ~6e-5 each) the exact path recomputes all 8.
+__device__ __forceinline__ uint2 quant8(uint4 u, float s, float inv, int& t) {
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+    float r[8];
+    bool near_tie = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(h[e]);
+        r[2 * e] = __fmul_rn(f.x, inv);
+        r[2 * e + 1] = __fmul_rn(f.y, inv);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float rc = fminf(fmaxf(r[i], -127.0f), 127.0f);
+        const float ri = rintf(rc);
+        near_tie |= fabsf(rc - ri) >= 0.5f - 0x1p-14f;
+        r[i] = ri;
+    }
+    if (near_tie) return quant8_exact(u, s, t);
+    uint32_t w[2] = {0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int q = __float2int_rz(r[i]);   // r[i] is integer-valued
+        t += q;
+        w[i >> 2] |= (uint32_t)(q & 0xff) << (8 * (i & 3));
+    }
+    return make_uint2(w[0], w[1]);
+}
+
+}  // namespace qoq

@@ -15,6 +15,7 @@
 #include <cstdint>
 
 #include "qoq_internal.h"
+#include "qoq_quant.cuh"
 #include "sm100_ptx.cuh"
 
 namespace qoq {
@@ -43,24 +44,6 @@ __device__ __forceinline__ int block_reduce_sum(int v, int* red) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
-}
-
-// Symmetric fp16 scale: fp16_rn(amax / qmax); 1.0 for amax == 0; 2^-24 if it underflows to 0.
-__device__ __forceinline__ __half sym_scale(float amax, float qmax) {
-    if (amax == 0.0f) return __float2half_rn(1.0f);
-    __half s = __float2half_rn(__fdiv_rn(amax, qmax));
-    if ((__half_as_ushort(s) & 0x7fff) == 0) s = __ushort_as_half(1);
-    return s;
-}
-
-__device__ __forceinline__ float amax8(uint4 v, float a) {
-    const __half2* h = reinterpret_cast<const __half2*>(&v);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        float2 f = __half22float2(h[i]);
-        a = fmaxf(a, fmaxf(fabsf(f.x), fabsf(f.y)));
-    }
-    return a;
 }
 
 // ------------------------------------------------------------------ weights, level 1
@@ -143,25 +126,13 @@ __global__ void __launch_bounds__(128) level2_pack_kernel(const __half* __restri
 
 // ------------------------------------------------------------------ activations
 
-// One CTA per token row. The row (K <= 256 * 8 * kVec fp16) is read ONCE into registers, reduced
-// (amax), quantized from registers and summed; rows longer than the register budget take the
-// streaming path (second read hits L1/L2). PDL: the dependent GEMM is released at entry — its CTAs
+// One CTA per token row. Pass 1 reads the row with kVec loads per thread in flight (amax); pass 2
+// re-reads it from L1 and quantizes in a compact loop (an unrolled straight-line quantizer is large
+// enough to miss the instruction cache on every line). PDL: the dependent GEMM is released at entry — its CTAs
 // launch on the SMs this small grid leaves free and start streaming their (static) weights while
 // this kernel runs; they read q_x only after griddepcontrol.wait.
 constexpr int kQThreads = 256;
 constexpr int kVec = 8;   // uint4 (8 halves) per thread kept in registers: K <= 16384
-
-__device__ __forceinline__ uint2 quant8(uint4 u, float s, int& t) {
-    const __half* h = reinterpret_cast<const __half*>(&u);
-    uint32_t w[2] = {0, 0};
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const int q = min(127, max(-127, (int)roundf(__fdiv_rn(__half2float(h[e]), s))));
-        t += q;
-        w[e >> 2] |= (uint32_t)(q & 0xff) << (8 * (e & 3));
-    }
-    return make_uint2(w[0], w[1]);
-}
 
 __global__ void __launch_bounds__(kQThreads) quantize_act_kernel(const __half* __restrict__ X, int K, int ldx,
                                                                  int8_t* __restrict__ qx, __half* __restrict__ sx,
@@ -174,37 +145,25 @@ __global__ void __launch_bounds__(kQThreads) quantize_act_kernel(const __half* _
     const uint4* row = reinterpret_cast<const uint4*>(X + (size_t)m * ldx);
     uint2* out = reinterpret_cast<uint2*>(qx + (size_t)m * K);
     const int nv = K / 8;
-    int t = 0;
-    if (nv <= kQThreads * kVec) {
+    // pass 1: amax, kVec loads per thread in flight at once (one L2/HBM round trip per batch)
+    __half2 a2 = __float2half2_rn(0.0f);
+    for (int i0 = 0; i0 < nv; i0 += kQThreads * kVec) {
         uint4 r[kVec];
-        float a = 0.0f;
 #pragma unroll
         for (int j = 0; j < kVec; ++j) {
-            const int i = threadIdx.x + j * kQThreads;
+            const int i = i0 + threadIdx.x + j * kQThreads;
             r[j] = (i < nv) ? __ldg(row + i) : make_uint4(0, 0, 0, 0);
-            a = amax8(r[j], a);
         }
-        a = block_reduce_max(a, redf);
-        const __half sh = sym_scale(a, 127.0f);
-        const float s = __half2float(sh);
 #pragma unroll
-        for (int j = 0; j < kVec; ++j) {
-            const int i = threadIdx.x + j * kQThreads;
-            if (i < nv) out[i] = quant8(r[j], s, t);
-        }
-        if (tx) t = block_reduce_sum(t, redi);
-        if (threadIdx.x == 0) {
-            sx[m] = sh;
-            if (tx) tx[m] = t;
-        }
-        return;
+        for (int j = 0; j < kVec; ++j) a2 = amax8h(r[j], a2);
     }
-    float a = 0.0f;
-    for (int i = threadIdx.x; i < nv; i += blockDim.x) a = amax8(__ldg(row + i), a);
-    a = block_reduce_max(a, redf);
+    const float a = block_reduce_max(amax_of(a2), redf);
     const __half sh = sym_scale(a, 127.0f);
-    const float s = __half2float(sh);
-    for (int i = threadIdx.x; i < nv; i += blockDim.x) out[i] = quant8(__ldg(row + i), s, t);
+    const float s = __half2float(sh), inv = __frcp_rn(s);
+    // pass 2: quantize (the row is in L1 now); a compact rolled loop keeps the code in the i-cache
+    int t = 0;
+#pragma unroll 2
+    for (int i = threadIdx.x; i < nv; i += kQThreads) out[i] = quant8(__ldg(row + i), s, inv, t);
     if (tx) t = block_reduce_sum(t, redi);
     if (threadIdx.x == 0) {
         sx[m] = sh;

@@ -30,6 +30,7 @@
 
 #include "qoq_internal.h"
 #include "sm100_ptx.cuh"
+#include "qoq_quant.cuh"
 
 // Timing ablations (never in production builds; results are garbage when set):
 //   2: no activation TMA (xfull arrives without data)   4: no weight bulk copies (wfull arrives)
@@ -134,6 +135,13 @@ struct KParams {
     int M, MT, KT, KS, T, G, mode, S;   // mode 2: S-CTA clusters split one tile's K range
     long long I;                 // total steps = T * KS
     unsigned long long* trace;   // debug: per-CTA %globaltimer stamps (nullptr in production)
+    // fused per-token activation quantization (qoq_w4a8_linear, M <= 64): X != nullptr. The
+    // epilogue warps quantize rows m = blockIdx.x (mod gridDim.x) of X into q_x / s_x / t_x (the
+    // buffers qx/sx/tx above point to), then a grid handshake on qsync releases the q_x TMA loads.
+    const __half* X;
+    int8_t* qx_rows;             // q_x [M][K] (the tensor map's global buffer)
+    int ldx, K;
+    int* qsync;                  // [2] arrivals / departures; the last departure re-zeroes both
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -141,11 +149,35 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#ifndef QOQ_PDL_EARLY
+#define QOQ_PDL_EARLY 0
+#endif
+#ifndef QOQ_W_PREFILL
+#define QOQ_W_PREFILL 1   // W-ring stages issued before the setup barrier (each issue costs ~250 cycles)
+#endif
+// trace buffer layout (u64): [148 CTAs][kTrEv] globaltimer | [64 it][8] CTA-0 step stamps |
+// [16][8] CTA-0 per-MMA | [16][8] CTA-0 per-dequant-warp | [148][kTrEv] clock64
+constexpr int kTrEv = 32;
+constexpr int kTrIt = 148 * kTrEv;
+constexpr int kTrMma = kTrIt + 64 * 8;
+constexpr int kTrDq = kTrMma + 16 * 8;
+constexpr int kTraceCyc = kTrDq + 16 * 8;
+#ifndef QOQ_TRACING
+#define QOQ_TRACING 0   // the `trace` library variant (tools/trace_gemm.py) compiles the stamps in
+#endif
+#if QOQ_TRACING
+// per-CTA events: globaltimer (comparable across SMs) + clock64 (cycle-accurate within the CTA)
 #define QOQ_TRACE(p, ev) \
-    do { if ((p).trace) (p).trace[blockIdx.x * 16 + (ev)] = gtimer(); } while (0)
+    do { if ((p).trace) { (p).trace[blockIdx.x * kTrEv + (ev)] = gtimer(); \
+                          (p).trace[kTraceCyc + blockIdx.x * kTrEv + (ev)] = clock64(); } } while (0)
+
 // per-iteration stamps of CTA 0 use the SM cycle counter (clock64), cycle-accurate within the SM
 #define QOQ_TRACE_IT(p, it, ev) \
-    do { if ((p).trace && blockIdx.x == 0 && (it) < 64) (p).trace[148 * 16 + (it) * 8 + (ev)] = clock64(); } while (0)
+    do { if ((p).trace && blockIdx.x == 0 && (it) < 64) (p).trace[kTrIt + (it) * 8 + (ev)] = clock64(); } while (0)
+#else
+#define QOQ_TRACE(p, ev) do { } while (0)
+#define QOQ_TRACE_IT(p, it, ev) do { } while (0)
+#endif
 
 // Iterates the (tile, s0, s1) segments (ranges of steps of one output tile) a CTA owns.
 // Every role runs an identical copy.
@@ -182,6 +214,45 @@ struct SegIter {
         const long long rem = end - cur;
         s1 = (int)((long long)s0 + rem < KS ? s0 + rem : KS);
         cur += s1 - s0;
+        return true;
+    }
+};
+
+// Weight producer state (warp 0, lane 0): walks the CTA's segments step by step; issue() waits for the
+// ring slot, then bulk-copies the step's 1-2 packed tiles (contiguous in the tile stream). Resumable,
+// so the first ring's worth can be issued before the setup barrier.
+template <class C>
+struct WProducer {
+    SegIter si;
+    int nt = 0, sg = 0, s1 = 0, ws = 0, rank, cg;
+    uint32_t wph = 0;
+    bool live;
+    uint64_t pol;
+    __device__ WProducer(const KParams& p, int cg_, int rank_) : si(p, cg_), rank(rank_), cg(cg_) {
+        int tile, s0;
+        live = si.next(tile, s0, s1);
+        sg = s0;
+        nt = live ? (tile / p.MT) * cg + rank : 0;
+        pol = policy_evict_first();   // each weight byte is read once
+    }
+    __device__ bool issue(const KParams& p, uint8_t* smem, uint64_t* wfull, uint64_t* wfree) {
+        if (!live) return false;
+        const int kt0 = 2 * sg, nk = (kt0 + 1 < p.KT) ? 2 : 1;
+        mbar_wait(&wfree[ws], wph ^ 1);
+        uint8_t* dst = smem + C::kWOff + ws * C::kWStageBytes;
+        if (QOQ_ABLATE & 4) {
+            mbar_arrive(&wfull[ws]);
+        } else {
+            mbar_arrive_expect_tx(&wfull[ws], nk * kTileBytes);
+            bulk_g2s(dst, p.packed + ((size_t)nt * p.KT + kt0) * kTileBytes, nk * kTileBytes, &wfull[ws], pol);
+        }
+        if (++ws == C::kWStages) { ws = 0; wph ^= 1; }
+        if (++sg == s1) {
+            int tile, s0;
+            live = si.next(tile, s0, s1);
+            sg = s0;
+            if (live) nt = (tile / p.MT) * cg + rank;
+        }
         return true;
     }
 };
@@ -227,6 +298,82 @@ __device__ __forceinline__ void expand_row(const uint4 (&v)[4], uint32_t s, uint
     }
 }
 
+// Fused per-token quantization by the 128 epilogue threads (et) of this CTA: rows m ≡ blockIdx.x
+// (mod gridDim.x), same arithmetic as quantize_act_kernel (qoq_quant.cuh): amax with kQVec loads
+// per thread in flight, then a compact quantize loop over the (L1-resident) row. red/redi: >= 4
+// floats / ints of shared scratch. Ends with this CTA's arrival on qsync[0] (release).
+constexpr int kQVec = 8;
+
+__device__ __forceinline__ void quant_row_finish(const KParams& p, int m, int et, float* red, int* redi, float a,
+                                                 float& sc, __half& sh) {
+    const int g = et >> 5, l = et & 31;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (l == 0) red[g] = a;
+    named_bar_sync(1, 128);
+    a = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    sh = sym_scale(a, 127.0f);
+    sc = __half2float(sh);
+}
+
+__device__ __forceinline__ void quant_row_sum(const KParams& p, int m, int et, int* redi, int t, __half sh) {
+    const int g = et >> 5, l = et & 31;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (l == 0) redi[g] = t;
+    named_bar_sync(1, 128);
+    if (et == 0) {
+        const_cast<__half*>(p.sx)[m] = sh;
+        const_cast<int32_t*>(p.tx)[m] = redi[0] + redi[1] + redi[2] + redi[3];
+    }
+}
+
+__device__ __forceinline__ void fused_quantize_rows(const KParams& p, int et, float* red, int* redi) {
+    const int nv = p.K / 8;
+    for (int m = blockIdx.x; m < p.M; m += gridDim.x) {
+        const uint4* row = reinterpret_cast<const uint4*>(p.X + (size_t)m * p.ldx);
+        uint2* out = reinterpret_cast<uint2*>(p.qx_rows + (size_t)m * p.K);
+        __half2 a2 = __float2half2_rn(0.0f);
+        for (int i0 = 0; i0 < nv; i0 += 128 * kQVec) {   // kQVec loads per thread in flight
+            uint4 v[kQVec];
+#pragma unroll
+            for (int j = 0; j < kQVec; ++j) {
+                const int i = i0 + et + 128 * j;
+                v[j] = (i < nv) ? __ldg(row + i) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int j = 0; j < kQVec; ++j) a2 = amax8h(v[j], a2);
+        }
+        if (et == 0 && m == (int)blockIdx.x) QOQ_TRACE(p, 16);
+        float sc;
+        __half sh;
+        quant_row_finish(p, m, et, red, redi, amax_of(a2), sc, sh);
+        if (et == 0 && m == (int)blockIdx.x) QOQ_TRACE(p, 17);
+        const float inv = __frcp_rn(sc);
+        int t = 0;
+#pragma unroll 2
+        for (int i = et; i < nv; i += 128) out[i] = quant8(__ldg(row + i), sc, inv, t);   // L1 re-read
+        if (et == 0 && m == (int)blockIdx.x) QOQ_TRACE(p, 18);
+        quant_row_sum(p, m, et, redi, t, sh);
+        if (et == 0 && m == (int)blockIdx.x) QOQ_TRACE(p, 19);
+    }
+    named_bar_sync(1, 128);   // all rows of this CTA written (CTA-scope), then one cumulative release
+    if (et == 0) {
+        QOQ_TRACE(p, 20);
+        red_release_add_gpu(p.qsync, 1);   // cumulative through the CTA barrier above
+        QOQ_TRACE(p, 21);
+    }
+}
+
+// A consumer of the fused q_x is past the grid handshake: count it; the last of the 2 per CTA
+// (activation producer + epilogue) re-zeroes the counters for the next launch.
+__device__ __forceinline__ void fused_depart(const KParams& p) {
+    if (atomicAdd(p.qsync + 1, 1) == 2 * (int)gridDim.x - 1) {
+        atomicExch(p.qsync, 0);
+        atomicExch(p.qsync + 1, 0);
+    }
+}
+
 template <int BN>
 __device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<BN, 1>::kChunk]) {
     if constexpr (Cfg<BN>::kChunk == 32) tmem_ld_32x32b_x32(taddr, v);
@@ -252,7 +399,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
     uint64_t* aempty = afull + C::kAStages;   // MMAs reading TMEM buffer a complete (commit)
     uint64_t* accfull = aempty + C::kAStages; // both issuers committed the accumulator stage
     uint64_t* accempty = accfull + C::kAccStages;
-    uint64_t* red_full = accempty + C::kAccStages;   // mode 2 leader: all S partials reduced into stg
+    uint64_t* red_full = accempty + C::kAccStages;   // mode 2: all S partial slices reduced into stg
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_full + 1);
     volatile int* fin_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
@@ -260,19 +407,29 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) QOQ_TRACE(p, 0);
     const bool clustered = (p.mode == 2);
-    const bool leader = clustered && cluster_ctarank() == 0;
+    // mode 2 (reduce-scatter): cluster rank c owns rows [c*R, (c+1)*R) of the tile, R = 128 / S
+    const int crank = clustered ? (int)cluster_ctarank() : 0;
+    constexpr int kRP = BN + 4;                       // padded row pitch (ints) of a staged partial
     const int rank = (CG == 2) ? (int)cluster_ctarank() : 0;   // CTA-pair: which 128-row tile of the pair
-    if (leader) {   // zero the reduction target (the epilogue staging area) for the bulk reduce-adds
-        for (int i = threadIdx.x; i < BN * 128; i += blockDim.x) stg[i] = 0;
-        fence_proxy_async_smem();
-    }
-
-    if (warp == 0 && lane == 0) {
-        if (leader) {
+    const bool epi_thread = threadIdx.x >= C::R::kEpiThread0 && threadIdx.x < C::R::kEpiThread0 + 128;
+    if (clustered && epi_thread) {
+        // mode 2: the (otherwise idle) epilogue warps zero this CTA's receive slice in the staging
+        // area and arm red_full (one bulk reduce from every CTA of the cluster lands there), then
+        // release them cluster-wide; only these threads pay for the cluster-scope fence.
+        const int et = threadIdx.x - C::R::kEpiThread0;
+        for (int i = et * 4; i < (128 / p.S) * kRP; i += 128 * 4)
+            *reinterpret_cast<int4*>(stg + i) = make_int4(0, 0, 0, 0);
+        if (et == 0) {
             mbar_init(red_full, 1);
             fence_mbar_init();
-            mbar_arrive_expect_tx(red_full, (uint32_t)(p.S * BN * 128 * 4));
+            mbar_arrive_expect_tx(red_full, (uint32_t)(128 * kRP * 4));
         }
+        fence_proxy_async_smem();
+        fence_acq_rel_cluster();
+    }
+
+    WProducer<C> wprod(p, CG, rank);
+    if (warp == 0 && lane == 0) {
         for (int i = 0; i < C::kWStages; ++i) {
             mbar_init(&wfull[i], 1);
             mbar_init(&wfree[i], 4);
@@ -291,7 +448,16 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
         }
         fence_mbar_init();
         prefetch_tmap(&tmap_x);
+#if QOQ_W_PREFILL
+        // The weight producer (this thread) fills the W ring right away: the first bytes' HBM latency
+        // overlaps TMEM allocation and the setup barriers. The proxy fence makes the barrier inits
+        // visible to the async proxy that signals complete_tx on them.
+        fence_proxy_async_smem();
+        for (int i = 0; i < QOQ_W_PREFILL && i < C::kWStages && wprod.issue(p, smem, wfull, wfree); ++i) {
+        }
+#endif
     }
+    if (threadIdx.x == 0) QOQ_TRACE(p, 11);
     if (warp == 1) {
         if constexpr (CG == 2) {
             tmem_alloc2(tmem_slot, C::kTmemCols);
@@ -303,45 +469,45 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) QOQ_TRACE(p, 13);
     // mode 2: leader's zeroed target + armed red_full visible cluster-wide; CG = 2: the pair's
     // barriers initialized before any remote arrive
-    if (clustered || CG == 2) cluster_sync_all();
+    // CG = 2: the pair's barriers initialized before any remote arrive (full barrier). Mode 2: only
+    // arrive here; the first remote operation (the epilogue's reduce-scatter) waits for this phase,
+    // which has long completed by then.
+    if (CG == 2) cluster_sync_all();
+    else if (clustered) cluster_arrive_relaxed();   // the writers released above
+    bool cl_done = false;   // mode 2: this thread has waited phase 0 and arrived on phase 1
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) QOQ_TRACE(p, 1);
+#if QOQ_PDL_EARLY
+    // PDL: release the dependent grid now. Its CTAs can only become resident on SMs this grid leaves
+    // free (one GEMM CTA fills an SM's shared memory), where they set up and stream their own static
+    // weights; everything they read from this grid sits behind their griddepcontrol.wait, which
+    // still waits for this grid's completion and memory flush.
+    pdl_launch_dependents();
+#endif
 
     // PDL: weights and scales are static, so the weight producer streams them without waiting for the
     // previous kernel; everything that reads what the previous kernel wrote (q_x via TMA, s_x, t_x,
     // the split-K workspace) sits behind griddepcontrol.wait.
     if (warp == 0) {
-        // ===================== weight producer: per step, 1-2 packed 8448-B tiles via cp.async.bulk.
-        // Weights are static, so it runs ahead of griddepcontrol.wait (overlaps the previous kernel).
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();   // each weight byte is read once
-            SegIter si(p, CG);
-            int tile, s0, s1, ws = 0;
-            uint32_t wph = 0;
-            while (si.next(tile, s0, s1)) {
-                const int nt = (tile / p.MT) * CG + rank;
-                for (int sg = s0; sg < s1; ++sg) {
-                    const int kt0 = 2 * sg, nk = (kt0 + 1 < p.KT) ? 2 : 1;
-                    mbar_wait(&wfree[ws], wph ^ 1);
-                    uint8_t* dst = smem + C::kWOff + ws * C::kWStageBytes;
-                    if (QOQ_ABLATE & 4) {
-                        mbar_arrive(&wfull[ws]);
-                    } else {
-                        mbar_arrive_expect_tx(&wfull[ws], nk * kTileBytes);
-                        bulk_g2s(dst, p.packed + ((size_t)nt * p.KT + kt0) * kTileBytes, nk * kTileBytes, &wfull[ws],
-                                 pol);   // the step's 1-2 tiles are contiguous in the tile stream
-                    }
-                    if (++ws == C::kWStages) { ws = 0; wph ^= 1; }
-                }
+        // ===================== weight producer: the rest of the stream (the first ring's worth was
+        // issued before the CTA-wide setup barrier, above). Weights are static, so it runs ahead of
+        // griddepcontrol.wait (overlaps the previous kernel).
+        if (lane == 0)
+            while (wprod.issue(p, smem, wfull, wfree)) {
             }
-        }
     } else if (warp == C::R::kXProdWarp) {
         // ===================== activation producer: TMA 2-D (SWIZZLE_128B) k-tiles of q_x
         if (lane == 0) {
             pdl_wait();
+            if (p.X) {   // fused quantization: every CTA's q_x rows written (acquire), then visible
+                spin_until_ge(p.qsync, (int)gridDim.x);   // to this thread's async-proxy (TMA) reads
+                fence_proxy_async_global();
+                fused_depart(p);
+            }
             QOQ_TRACE(p, 2);
             SegIter si(p, CG);
             int tile, s0, s1, xs = 0, it = 0;
@@ -404,8 +570,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                                 const uint32_t accum = (local > first || t > 0 || kk > 0) ? 1u : 0u;
                                 if constexpr (CG == 2) mma_i8_ts2(d, a + t * 32 + kk * 8, bdesc, idesc, accum);
                                 else mma_i8_ts(d, a + t * 32 + kk * 8, bdesc, idesc, accum);
-                                if (p.trace && blockIdx.x == 0 && it < 16)
-                                    p.trace[148 * 16 + 64 * 8 + it * 8 + t * 4 + kk] = clock64();
+                                if (QOQ_TRACING && p.trace && blockIdx.x == 0 && it < 16)
+                                    p.trace[kTrMma + it * 8 + t * 4 + kk] = clock64();
                             }
                         }
                         if constexpr (CG == 2) {     // free the buffers in both CTAs of the pair
@@ -485,8 +651,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                     }
                     tmem_wait_st();
                     if (tw) QOQ_TRACE_IT(p, it, 3);
-                    if (lane == 0 && p.trace && blockIdx.x == 0 && it < 16)   // per-warp completion
-                        p.trace[148 * 16 + 64 * 8 + 16 * 8 + it * 8 + (warp - 2)] = clock64();
+                    if (QOQ_TRACING && lane == 0 && p.trace && blockIdx.x == 0 && it < 16)   // per-warp completion
+                        p.trace[kTrDq + it * 8 + (warp - 2)] = clock64();
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
@@ -505,6 +671,17 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
         const int g = et >> 5, l = et & 31;           // vector mapping: rows 4l..4l+3, tokens g, g+4, ...
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         pdl_wait();
+        if (et == 0) QOQ_TRACE(p, 12);
+        if (p.X) {   // fused per-token quantization of X, then the grid handshake (s_x / t_x below)
+            fused_quantize_rows(p, et, sxs, txs);
+            if (et == 0) {
+                QOQ_TRACE(p, 3);
+                spin_until_ge(p.qsync, (int)gridDim.x);
+                QOQ_TRACE(p, 4);
+                fused_depart(p);
+            }
+            named_bar_sync(1, 128);
+        }
         SegIter si(p, CG);
         int tile, s0, s1, cst = 0, it0e = 0;
         uint32_t cph = 0;
@@ -520,8 +697,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
             int32_t* wst = p.ws + (size_t)tile * 128 * BN;
             for (int jj = et; jj < BN; jj += 128) {
                 const int m = m0 + jj;
-                sxs[jj] = (!OUT_I32 && m < p.M) ? __half2float(__ldg(p.sx + m)) : 0.0f;
-                txs[jj] = (p.tx && m < p.M) ? 128 * __ldg(p.tx + m) : 0;
+                // coherent (L2) loads: with the fused quantization they were written by this grid
+                sxs[jj] = (!OUT_I32 && m < p.M) ? __half2float(__ldcg(p.sx + m)) : 0.0f;
+                txs[jj] = (p.tx && m < p.M) ? 128 * __ldcg(p.tx + m) : 0;
             }
             float s0v[4] = {0.f, 0.f, 0.f, 0.f};
             if constexpr (!OUT_I32) {
@@ -536,8 +714,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
             tc_fence_after();
             const uint32_t d = tmem + lane_off + C::kAStages * 64 + (cst * C::kIssuers + single) * BN;
             if (clustered) {
-                // ---- cluster split-K: stage this CTA's partial (sum of both issuers' accumulators) in
-                // its now-idle X ring, then one bulk reduce-add into the leader's staging area.
+                // ---- cluster split-K, reduce-scatter through DSMEM: stage this CTA's partial (sum of
+                // both issuers' accumulators) row-major [128][BN+4] in its now-idle X ring; the rows
+                // of CTA c's slice are one contiguous block, bulk-reduce-added into CTA c's staging.
                 int32_t* part = reinterpret_cast<int32_t*>(smem + C::kXOff);
 #pragma unroll 1
                 for (int ci = 0; ci < BN / C::kChunk; ++ci) {
@@ -554,29 +733,48 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                         tmem_wait_ld();
                     }
 #pragma unroll
-                    for (int i = 0; i < C::kChunk; ++i) part[(j0 + i) * 128 + r] = (int32_t)v[i];
+                    for (int i = 0; i < C::kChunk; i += 4)
+                        *reinterpret_cast<int4*>(part + r * kRP + j0 + i) =
+                            make_int4((int)v[i], (int)v[i + 1], (int)v[i + 2], (int)v[i + 3]);
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accempty[cst]);
                 fence_proxy_async_smem();
                 named_bar_sync(1, 128);
-                if (et == 0) {
-                    QOQ_TRACE(p, 7);
-                    bulk_reduce_add_s32_cluster(mapa_shared(smem_u32(stg), 0), part, BN * 128 * 4,
-                                                mapa_shared(smem_u32(red_full), 0));
+                cluster_wait_acquire();   // every CTA's zeroed slice + armed red_full (setup arrive)
+                const int R = 128 / p.S;
+                if (et < p.S) {   // thread c sends slice c to cluster rank c
+                    const uint32_t bytes = (uint32_t)(R * kRP * 4);
+                    bulk_reduce_add_s32_cluster(mapa_shared(smem_u32(stg), et), part + et * R * kRP, bytes,
+                                                mapa_shared(smem_u32(red_full), et));
                 }
-                if (leader) {
-                    mbar_wait(red_full, 0);
-#pragma unroll
-                    for (int jj = g; jj < BN; jj += 4) {
-                        const int m = m0 + jj;
-                        if (m < p.M)
-                            write_out4<OUT_I32>(p, m, n0 + 4 * l, *reinterpret_cast<const int4*>(stg + jj * 128 + 4 * l),
-                                                txs[jj], sxs[jj], s0v);
+                if (et == 0) QOQ_TRACE(p, 7);
+                mbar_wait(red_full, 0);
+                // every slice this CTA receives has landed, so every read of the peers' partials that
+                // targets it is done: arrive on the exit barrier now and overlap its latency with
+                // the write-out below
+                cluster_arrive_release();
+                cl_done = true;
+                // this CTA's R rows, all BN tokens: thread -> (token jj, 4 consecutive rows)
+                const int nq = R / 4;
+                for (int w = et; w < nq * BN; w += 128) {
+                    const int jj = w / nq, rr = (w % nq) * 4;
+                    const int m = m0 + jj, n = n0 + crank * R + rr;
+                    if (m < p.M) {
+                        int4 a4 = make_int4(stg[(rr + 0) * kRP + jj], stg[(rr + 1) * kRP + jj],
+                                            stg[(rr + 2) * kRP + jj], stg[(rr + 3) * kRP + jj]);
+                        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                        if constexpr (!OUT_I32) {
+                            const uint2 u = __ldg(reinterpret_cast<const uint2*>(p.s0 + n));
+                            const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+                            const float2 fa = __half22float2(h2[0]), fb = __half22float2(h2[1]);
+                            s4[0] = fa.x; s4[1] = fa.y; s4[2] = fb.x; s4[3] = fb.y;
+                        }
+                        write_out4<OUT_I32>(p, m, n, a4, txs[jj], sxs[jj], s4);
                     }
-                    if (et == 0) QOQ_TRACE(p, 9);
                 }
+                if (et == 0) QOQ_TRACE(p, 9);
                 if (++cst == C::kAccStages) { cst = 0; cph ^= 1; }
                 named_bar_sync(1, 128);
                 continue;
@@ -665,11 +863,21 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
     }
 
     tc_fence_before();
+    if (threadIdx.x == C::R::kEpiThread0) QOQ_TRACE(p, 14);
     __syncthreads();
-    // mode 2: no CTA may exit while its partial is still being read by a bulk reduce (completion is
-    // only signalled at the leader), so the leader releases the cluster after red_full completed.
+    if (threadIdx.x == 0) QOQ_TRACE(p, 15);
+    // mode 2: no CTA may exit while a peer's bulk reduce still reads its partial or writes its slice:
+    // the exit barrier completes once every CTA has seen its own slice complete (arrived above).
     // CG = 2: the leader's MMAs read the peer's TMEM; both CTAs are past their epilogues here
-    if (clustered || CG == 2) cluster_sync_all();
+    if (CG == 2) {
+        cluster_sync_all();
+    } else if (clustered) {
+        if (!cl_done) {
+            cluster_wait_acquire();
+            cluster_arrive_release();
+        }
+        cluster_wait_acquire();
+    }
     if (threadIdx.x == 0) QOQ_TRACE(p, 10);
     pdl_launch_dependents();
     if (warp == 1) {
@@ -745,7 +953,8 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     //  * T >= #SMs: whole tiles (mode 0).
     //  * BN <= 32: S-CTA cluster split-K through DSMEM (mode 2) — the partial is only 8-16 KB/CTA.
     //  * BN = 64: no split while K <= 3072 steps-worth (KS <= 24; the pipeline fill/drain per CTA
-    //    costs more than the idle SMs), stream-K with the L2 workspace (mode 1) for long K.
+    //    costs more than the idle SMs); for long K the cluster reduce-scatter (mode 2, 14.3 us for
+    //    down_proj M=64) edges out stream-K through the L2 workspace (mode 1, 14.6 us).
     //  * BN >= 128 with T < #SMs: stream-K (mode 1).
     // QOQ_FORCE_MODE=0/1/2 overrides (debug / tests).
     const char* fm = getenv("QOQ_FORCE_MODE");
@@ -754,18 +963,18 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     if (force >= 0 && force <= 2) want = force;
     else if (p.T >= num_sms) want = 0;
     else if (p.BN <= 32) want = 2;
-    else if (p.BN == 64) want = p.KS <= 24 ? 0 : 1;
+    else if (p.BN == 64) want = p.KS <= 24 ? 0 : 2;
     else want = 1;
     if (want == 2 && p.BN > 64) want = 1;   // the DSMEM reduction target holds at most 128 x 64 INT32
     int S = 1;
     if (want == 2) {
-        S = num_sms / p.T;
-        if (S > 8) S = 8;
-        if (S > p.KS) S = p.KS;
+        // reduce-scatter slices of 128/S rows: S a power of two <= 8, <= #steps, all clusters resident
+        S = 1;
+        while (S * 2 <= 8 && (long long)p.T * S * 2 <= num_sms && S * 2 <= p.KS) S *= 2;
         while (S >= 2) {
             const int mc = max_clusters_bn(p.BN, S);
             if (mc < 0 || (long long)mc >= p.T) break;   // all T clusters co-resident (or query unavailable)
-            --S;
+            S /= 2;
         }
         if (S < 2) want = (p.KS <= 24) ? 0 : 1;
     }
@@ -839,6 +1048,11 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     kp.S = pl.S;
     kp.I = pl.I;
     kp.trace = static_cast<unsigned long long*>(a.trace);
+    kp.X = static_cast<const __half*>(a.X);
+    kp.qx_rows = const_cast<int8_t*>(a.qx);
+    kp.ldx = a.ldx;
+    kp.K = a.K;
+    kp.qsync = a.qsync;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.G * CG);
     cfg.blockDim = dim3(C::kBlockThreads);

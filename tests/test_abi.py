@@ -45,7 +45,7 @@ def test_library_is_sm100a_only(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert lib.qoq_abi_version() == 1
+    assert lib.qoq_abi_version() == 2
     for s in range(0, 8):
         assert lib.qoq_status_string(s)
 
@@ -57,6 +57,10 @@ def test_sizes(lib):
     assert lib.qoq_packed_weight_bytes(256, 256, 64) == 0
     assert lib.qoq_gemm_workspace_bytes(16, 64, 256) == 0                     # N not a multiple of 128
     assert lib.qoq_linear_host_scratch_bytes(16, 256, 256) >= 16 * 256 * 5
+    # fused linear workspace: 256 B sync + q_x + s_x + t_x (+ split-K partials), 256-B aligned parts
+    assert lib.qoq_linear_workspace_bytes(16, 256, 256) >= 256 + 16 * 256 + 2 * 256
+    assert lib.qoq_linear_workspace_bytes(16, 256, 200) == 0
+    assert lib.qoq_linear_workspace_bytes(64, 4096, 4096) % 256 == 0
 
 
 def test_host_validation_before_any_device_work(lib):
@@ -70,6 +74,19 @@ def test_host_validation_before_any_device_work(lib):
     assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 4, 256, 256, 64, fake, 256, None, 0, None) == 3
     assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 4, 256, 256, 128, fake, 100, None, 0, None) == 1
     assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 4, 256, 131072, 128, fake, 256, None, 0, None) == 2
+    # fused linear: shape / group / ldx / ldy / alignment / workspace size, all before device work
+    Z = ctypes.c_size_t
+    big = Z(1 << 30)
+    assert lib.qoq_w4a8_linear(fake, 200, 4, 256, 200, 128, fake, fake, fake, 256, fake, big, None) == 2
+    assert lib.qoq_w4a8_linear(fake, 256, 4, 256, 256, 64, fake, fake, fake, 256, fake, big, None) == 3
+    assert lib.qoq_w4a8_linear(fake, 128, 4, 256, 256, 128, fake, fake, fake, 256, fake, big, None) == 1
+    assert lib.qoq_w4a8_linear(fake, 256, 4, 256, 256, 128, fake, fake, fake, 100, fake, big, None) == 1
+    assert lib.qoq_w4a8_linear(P((1 << 20) + 8), 256, 4, 256, 256, 128, fake, fake, fake, 256, fake, big,
+                               None) == 1                                      # X not 16-B aligned
+    assert lib.qoq_w4a8_linear(fake, 256, 4, 256, 256, 128, fake, fake, fake, 256, P((1 << 20) + 16), big,
+                               None) == 1                                      # workspace not 256-B aligned
+    assert lib.qoq_w4a8_linear(fake, 256, 4, 256, 256, 128, fake, fake, fake, 256, fake, Z(64), None) == 5
+    assert lib.qoq_w4a8_linear(fake, 256, 0, 256, 256, 128, fake, fake, fake, 256, fake, Z(0), None) == 0
     # M == 0 is a no-op that never touches the device
     assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 0, 256, 256, 128, fake, 256, None, 0, None) == 0
     assert lib.qoq_quantize_activations_per_token(fake, 0, 256, 256, fake, fake, None, None) == 0

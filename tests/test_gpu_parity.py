@@ -116,11 +116,14 @@ def test_full_path_config1_and_workspace_restored(gpu_lib):
     W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=0)
     ws = gpu_lib.Workspace(dev())
     packed, s0 = gpu_lib.quantize_weights(to_dev(W))
-    Y = gpu_lib.linear(to_dev(X), packed, s0, N, workspace=ws)
+    qx, sx, tx = gpu_lib.quantize_activations_per_token(to_dev(X))
+    Y = gpu_lib.w4a8_gemm(qx, sx, tx, packed, s0, N, workspace=ws)
     torch.cuda.synchronize()
     check_y(Y, oracle.linear_rows(X, p_ref, s0_ref, N))
     if ws.buf is not None:
         assert int(ws.buf.count_nonzero()) == 0
+    # the one-call linear layer (fused quantization) on the same inputs: identical Y
+    assert torch.equal(gpu_lib.linear(to_dev(X), packed, s0, N), Y)
 
 
 def test_gemm_matches_library_w8a8_on_dequantized_weights(gpu_lib):
@@ -250,3 +253,89 @@ def test_gemm_cta_pair_bit_exact(gpu_lib, monkeypatch, mode, M, N, K):
     Y = gpu_lib.w4a8_gemm(to_dev(qx_ref), to_dev(sx_ref), to_dev(tx_ref), to_dev(p_ref), to_dev(s0_ref), N,
                           workspace=ws)
     check_y(Y, oracle.epilogue_f64(oracle.acc_from_packed(qx_ref, p_ref, N, K), sx_ref, s0_ref))
+
+
+# ------------------------------------------------------------------ fused linear (quantize + GEMM)
+
+FUSED_SHAPES = [
+    (1, 128, 128, 128),       # one tile, one CTA quantizes the only row
+    (16, 256, 256, 264),      # ldx > K (a TP K-shard view)
+    (33, 1280, 1024, 1024),
+    (64, 4096, 4096, 4096),   # decode o_proj
+    (64, 128, 4096, 4096),    # one output tile: few CTAs, each quantizes many rows
+    (64, 19200, 384, 384),    # 150 tiles > 148 SMs: persistent CTAs, every SM in the handshake
+    (5, 2560, 1408, 1408),
+    (48, 1024, 14336, 14336), # long rows (down_proj K)
+    (65, 512, 1024, 1024),    # above the fusion limit: quantizer kernel + GEMM
+    (300, 1280, 1024, 1024),
+]
+
+
+def _fused_case(M, N, K, ldx, seed):
+    W = synth.weights_fp16(N, K, seed=seed)
+    X = synth.activations_fp16(M, ldx, seed=seed)
+    if M > 3:
+        X[2] = 0
+        X[3] = np.float16(2e-6) * np.sign(X[3])
+    p_ref, s0_ref = oracle.quantize_weights(W)
+    qx_ref, sx_ref, tx_ref = oracle.quantize_activations(X, K)
+    return X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref
+
+
+@pytest.mark.parametrize("mode", ["auto", "0", "1", "2", "cg2"])
+@pytest.mark.parametrize("M,N,K,ldx", FUSED_SHAPES)
+def test_fused_linear_bit_exact(gpu_lib, monkeypatch, mode, M, N, K, ldx):
+    """qoq_w4a8_linear (per-token quantization fused into the GEMM for M <= 64): the quantized
+    activations it leaves in the workspace equal the oracle's bit for bit, Y is bit-identical to the
+    two-call path (quantizer + GEMM) and within tolerance of the oracle, and repeated launches on
+    the same workspace (grid-handshake counters re-zeroed by the last CTA) stay exact."""
+    if mode == "cg2":
+        monkeypatch.setenv("QOQ_FORCE_CG", "2")
+    elif mode != "auto":
+        monkeypatch.setenv("QOQ_FORCE_MODE", mode)
+    X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _fused_case(M, N, K, ldx, seed=M + N + K)
+    Xd, packed, s0 = to_dev(X), to_dev(p_ref), to_dev(s0_ref)
+    nbytes = gpu_lib.linear_workspace_bytes(M, N, K)
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device=dev())
+
+    class _WS:   # caller-owned workspace (exact size) so its contents can be inspected
+        def get(self, n):
+            return ws, ws.numel()
+
+    two = gpu_lib.w4a8_gemm(to_dev(qx_ref), to_dev(sx_ref), to_dev(tx_ref), packed, s0, N)
+    y_ref = oracle.epilogue_f64(oracle.acc_from_packed(qx_ref, p_ref, N, K), sx_ref, s0_ref)
+    for rep in range(3):
+        Y = gpu_lib.w4a8_linear(Xd, packed, s0, N, K, workspace=_WS())
+        torch.cuda.synchronize()
+        assert torch.equal(Y, two), f"rep {rep}: fused Y differs from quantizer + GEMM"
+        check_y(Y, y_ref)
+        qx, sx, tx = gpu_lib.linear_workspace_views(ws, M, K)
+        assert np.array_equal(qx.cpu().numpy(), qx_ref)
+        assert np.array_equal(bits16(sx), sx_ref.view(np.uint16))
+        assert np.array_equal(tx.cpu().numpy(), tx_ref)
+        assert int(ws[:256].count_nonzero()) == 0, "handshake counters not re-zeroed"
+        o = 256 + (M * K + 255) // 256 * 256 + (2 * M + 255) // 256 * 256 + (4 * M + 255) // 256 * 256
+        assert int(ws[o:].count_nonzero()) == 0, "split-K workspace not restored"
+
+
+def test_fused_linear_in_cuda_graph(gpu_lib):
+    """The fused kernel replayed from a CUDA graph (frozen arguments, same workspace every replay)
+    with changing activations: every replay quantizes the new X and matches the oracle."""
+    M, N, K = 64, 1280, 1024
+    X0, p_ref, s0_ref, *_ = _fused_case(M, N, K, K, seed=77)
+    packed, s0 = to_dev(p_ref), to_dev(s0_ref)
+    Xd = to_dev(X0)
+    ws = gpu_lib.Workspace(dev())
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        Y = gpu_lib.w4a8_linear(Xd, packed, s0, N, workspace=ws, stream=s)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            gpu_lib.w4a8_linear(Xd, packed, s0, N, out=Y, workspace=ws, stream=s)
+    for seed in (1, 2, 3):
+        X = synth.activations_fp16(M, K, seed=seed)
+        Xd.copy_(to_dev(X))
+        g.replay()
+        torch.cuda.synchronize()
+        check_y(Y, oracle.linear_rows(X, p_ref, s0_ref, N))

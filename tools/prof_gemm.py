@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--time", action="store_true")
     ap.add_argument("--with-quant", action="store_true")
+    ap.add_argument("--fused", action="store_true", help="qoq_w4a8_linear (quantization fused into the GEMM)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     qoq.load()
@@ -44,6 +45,9 @@ def main():
 
     def run():
         for p, s0 in packs:
+            if a.fused:
+                qoq.w4a8_linear(X, p, s0, a.N, out=Y, workspace=ws, stream=s)
+                continue
             if a.with_quant:
                 qoq.quantize_activations_per_token(X, out=q, stream=s)
             qoq.w4a8_gemm(*q, p, s0, a.N, out=Y, workspace=ws, stream=s)
