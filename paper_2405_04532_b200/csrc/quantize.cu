@@ -126,13 +126,14 @@ __global__ void __launch_bounds__(128) level2_pack_kernel(const __half* __restri
 
 // ------------------------------------------------------------------ activations
 
-// One CTA per token row. Pass 1 reads the row with kVec loads per thread in flight (amax); pass 2
-// re-reads it from L1 and quantizes in a compact loop (an unrolled straight-line quantizer is large
-// enough to miss the instruction cache on every line). PDL: the dependent GEMM is released at entry — its CTAs
-// launch on the SMs this small grid leaves free and start streaming their (static) weights while
-// this kernel runs; they read q_x only after griddepcontrol.wait.
+// One CTA per token row: the row (K <= 8 * kQThreads * kQVec) is read ONCE into registers with all
+// loads in flight, reduced (amax, half2), quantized from registers (division-free, qoq_quant.cuh) and
+// summed; longer rows stream with a second (L1/L2) read. 64 rows at decode leave most SMs free for
+// the dependent GEMM, which PDL releases at entry: its CTAs stream their static weights while this
+// kernel runs and read q_x only after griddepcontrol.wait. (Measured on the decode step: splitting
+// rows over clusters to use more SMs, or capping registers to co-reside with GEMM CTAs, was slower.)
 constexpr int kQThreads = 256;
-constexpr int kVec = 8;   // uint4 (8 halves) per thread kept in registers: K <= 16384
+constexpr int kQVec = 8;
 
 __global__ void __launch_bounds__(kQThreads) quantize_act_kernel(const __half* __restrict__ X, int K, int ldx,
                                                                  int8_t* __restrict__ qx, __half* __restrict__ sx,
@@ -145,25 +146,32 @@ __global__ void __launch_bounds__(kQThreads) quantize_act_kernel(const __half* _
     const uint4* row = reinterpret_cast<const uint4*>(X + (size_t)m * ldx);
     uint2* out = reinterpret_cast<uint2*>(qx + (size_t)m * K);
     const int nv = K / 8;
-    // pass 1: amax, kVec loads per thread in flight at once (one L2/HBM round trip per batch)
-    __half2 a2 = __float2half2_rn(0.0f);
-    for (int i0 = 0; i0 < nv; i0 += kQThreads * kVec) {
-        uint4 r[kVec];
+    int t = 0;
+    __half sh;
+    if (nv <= kQThreads * kQVec) {
+        uint4 r[kQVec];
 #pragma unroll
-        for (int j = 0; j < kVec; ++j) {
-            const int i = i0 + threadIdx.x + j * kQThreads;
+        for (int j = 0; j < kQVec; ++j) {
+            const int i = threadIdx.x + j * kQThreads;
             r[j] = (i < nv) ? __ldg(row + i) : make_uint4(0, 0, 0, 0);
         }
+        __half2 a2 = __float2half2_rn(0.0f);
 #pragma unroll
-        for (int j = 0; j < kVec; ++j) a2 = amax8h(r[j], a2);
+        for (int j = 0; j < kQVec; ++j) a2 = amax8h(r[j], a2);
+        sh = sym_scale(block_reduce_max(amax_of(a2), redf), 127.0f);
+        const float s = __half2float(sh), inv = __frcp_rn(s);
+#pragma unroll
+        for (int j = 0; j < kQVec; ++j) {
+            const int i = threadIdx.x + j * kQThreads;
+            if (i < nv) out[i] = quant8(r[j], s, inv, t);
+        }
+    } else {
+        __half2 a2 = __float2half2_rn(0.0f);
+        for (int i = threadIdx.x; i < nv; i += kQThreads) a2 = amax8h(__ldg(row + i), a2);
+        sh = sym_scale(block_reduce_max(amax_of(a2), redf), 127.0f);
+        const float s = __half2float(sh), inv = __frcp_rn(s);
+        for (int i = threadIdx.x; i < nv; i += kQThreads) out[i] = quant8(__ldg(row + i), s, inv, t);
     }
-    const float a = block_reduce_max(amax_of(a2), redf);
-    const __half sh = sym_scale(a, 127.0f);
-    const float s = __half2float(sh), inv = __frcp_rn(s);
-    // pass 2: quantize (the row is in L1 now); a compact rolled loop keeps the code in the i-cache
-    int t = 0;
-#pragma unroll 2
-    for (int i = threadIdx.x; i < nv; i += kQThreads) out[i] = quant8(__ldg(row + i), s, inv, t);
     if (tx) t = block_reduce_sum(t, redi);
     if (threadIdx.x == 0) {
         sx[m] = sh;

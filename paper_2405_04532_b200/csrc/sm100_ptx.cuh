@@ -146,6 +146,16 @@ __device__ __forceinline__ void spin_until_ge(const int* p, int target) {
         if (n == (1u << 26)) __trap();
 }
 
+// 32-bit loads / stores to (possibly remote) cluster shared memory (address from mapa_shared)
+__device__ __forceinline__ uint32_t ld_shared_cluster_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_shared_cluster_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // Split cluster barrier (per thread, not warp-aligned): arrive (release) now, wait (acquire) later.
 __device__ __forceinline__ void cluster_arrive_release() {
     asm volatile("barrier.cluster.arrive.release;" ::: "memory");
