@@ -443,8 +443,9 @@ def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stre
     for name, N, K, kind, qg in shapes:
         Xh[name] = (torch.randn(M, K, generator=gen) * 1.0).half().pin_memory()
         Yh[name] = torch.empty(M, N, dtype=torch.float16).pin_memory()
-    scratch = torch.zeros(max(qoq.linear_host_scratch_bytes(M, N, K) for _, N, K, _, _ in shapes),
-                          dtype=torch.uint8, device=dev)
+    # one scratch per projection shape (the header's workspace-reuse rule), shared by all layers
+    scratch = {name: torch.zeros(qoq.linear_host_scratch_bytes(M, N, K), dtype=torch.uint8, device=dev)
+               for name, N, K, _, _ in shapes}
     h2d = sum(M * K * 2 for _, N, K, _, _ in shapes) * layers
     d2h = sum(M * N * 2 for _, N, K, _, _ in shapes) * layers
     red = {name: torch.empty(M, N, dtype=torch.float16, device=dev)
@@ -454,7 +455,7 @@ def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stre
         for l in range(layers):
             for i, (name, N, K, kind, qg) in enumerate(shapes):
                 p, s0 = packed[l][i]
-                qoq.linear_host(Xh[name], p, s0, N, Yh[name], scratch, stream=stream)
+                qoq.linear_host(Xh[name], p, s0, N, Yh[name], scratch[name], stream=stream)
                 if kind == "row" and world > 1:
                     with torch.cuda.stream(stream):
                         red[name].copy_(Yh[name], non_blocking=True)

@@ -114,8 +114,11 @@ int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed,
  *   qoq_quantize_weights.  Y_fp16 [M][ldy], ldy >= N, ldy % 4 == 0.
  * workspace: qoq_linear_workspace_bytes(M,N,K) bytes, 256-byte aligned, ZERO-FILLED before first
  * use; each call leaves its synchronization words and split-K partials zeroed again. Layout, each
- * part 256-byte aligned: [256 B sync][q_x int8 M*K][s_x fp16 M][t_x int32 M][GEMM workspace];
- * after the call q_x / s_x / t_x hold this call's quantized activations. One workspace per stream.
+ * part 256-byte aligned: [256 B sync][GEMM workspace, qoq_gemm_workspace_bytes(M,N,K)]
+ * [q_x int8 M*K][s_x fp16 M][t_x int32 M]; after the call q_x / s_x / t_x hold this call's
+ * quantized activations. One workspace per stream. Reusing a workspace for another shape is safe
+ * when both shapes have the same qoq_gemm_workspace_bytes (the zero-required parts then coincide);
+ * otherwise give each shape its own workspace (or re-zero it).
  * Same shape requirements as qoq_w4a8_gemm. */
 size_t qoq_linear_workspace_bytes(int M, int N, int K);
 int qoq_w4a8_linear(const void* X_fp16, int ldx, int M, int N, int K, int group,
@@ -126,8 +129,10 @@ int qoq_w4a8_linear(const void* X_fp16, int ldx, int M, int N, int K, int group,
 /* End-to-end linear layer with HOST activations (the e2e measurement path): copies X_host
  * (pinned host memory, [M][K] fp16) to the device, runs qoq_w4a8_linear against device-resident
  * packed weights and copies Y back to Y_host ([M][N] fp16, pinned).
- * dev_scratch: qoq_linear_host_scratch_bytes(M,N,K) bytes of device memory, zero-filled
- * before first use (it embeds the GEMM workspace). Asynchronous on `stream`. */
+ * dev_scratch: qoq_linear_host_scratch_bytes(M,N,K) bytes of device memory (256-byte aligned),
+ * zero-filled before first use. Layout: [linear workspace][X M*K fp16][Y M*N fp16], so the
+ * workspace rules of qoq_w4a8_linear (including reuse across shapes) apply to it. Asynchronous
+ * on `stream`. */
 size_t qoq_linear_host_scratch_bytes(int M, int N, int K);
 int qoq_linear_host(const void* X_host_fp16, int M, int K,
                     const void* packed, const void* s0_fp16, int N,

@@ -111,11 +111,12 @@ def linear_workspace_bytes(M: int, N: int, K: int) -> int:
     return load().qoq_linear_workspace_bytes(M, N, K)
 
 
-def linear_workspace_views(ws: torch.Tensor, M: int, K: int):
-    """(qx [M][K] int8, sx [M] fp16, tx [M] int32) views of a qoq_w4a8_linear workspace (header layout)."""
+def linear_workspace_views(ws: torch.Tensor, M: int, N: int, K: int):
+    """(qx [M][K] int8, sx [M] fp16, tx [M] int32) views of a qoq_w4a8_linear workspace (header layout:
+    [256 B sync][GEMM workspace][q_x][s_x][t_x], each part 256-B aligned)."""
     def up(v):
         return (v + 255) // 256 * 256
-    o_qx = 256
+    o_qx = 256 + up(gemm_workspace_bytes(M, N, K))
     o_sx = o_qx + up(M * K)
     o_tx = o_sx + up(2 * M)
     qx = ws[o_qx:o_qx + M * K].view(torch.int8).view(M, K)

@@ -59,7 +59,9 @@ int run_gemm(const int8_t* qx, const void* sx, const int32_t* tx, const void* pa
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// qoq_w4a8_linear workspace: [qsync 2 x int32][q_x M*K][s_x 2M][t_x 4M][GEMM workspace], 256-B aligned
+// qoq_w4a8_linear workspace: [qsync 2 x int32][GEMM workspace][q_x M*K][s_x 2M][t_x 4M], 256-B aligned.
+// The parts that must be zero at entry (sync words, split-K partials) come first, at offsets that do not
+// depend on K, so a workspace shared by several shapes keeps its sync words at offset 0.
 struct LinearWs {
     int* qsync;
     int8_t* qx;
@@ -74,12 +76,12 @@ LinearWs linear_ws_layout(void* base, int M, int N, int K) {
     uint8_t* b = static_cast<uint8_t*>(base);
     size_t off = 0;
     w.qsync = reinterpret_cast<int*>(b + off);  off += 256;
+    w.gemm_ws_bytes = plan_gemm(M, N, K, num_sms_or_default()).ws_bytes;
+    w.gemm_ws = b + off;                         off += align_up(w.gemm_ws_bytes, 256);
     w.qx = reinterpret_cast<int8_t*>(b + off);  off += align_up((size_t)M * K, 256);
     w.sx = b + off;                              off += align_up((size_t)M * 2, 256);
     w.tx = reinterpret_cast<int32_t*>(b + off); off += align_up((size_t)M * 4, 256);
-    w.gemm_ws = b + off;
-    w.gemm_ws_bytes = plan_gemm(M, N, K, num_sms_or_default()).ws_bytes;
-    w.total = off + align_up(w.gemm_ws_bytes, 256);
+    w.total = off;
     return w;
 }
 
@@ -202,10 +204,11 @@ int qoq_debug_w4a8_linear_trace(const void* X, int M, int N, int K, const void* 
     return run_linear(X, K, M, N, K, 128, packed, s0, Y, N, ws, ws_bytes, static_cast<cudaStream_t>(stream), trace);
 }
 
-// scratch layout: [X fp16 M*K][Y fp16 M*N][linear workspace], each 256-B aligned
+// scratch layout: [linear workspace][X fp16 M*K][Y fp16 M*N], each 256-B aligned (the zero-required
+// sync words sit at offset 0 whatever the shape)
 size_t qoq_linear_host_scratch_bytes(int M, int N, int K) {
     if (gemm_shape_status(M, N, K, 128) != QOQ_OK) return 0;
-    return align_up((size_t)M * K * 2, 256) + align_up((size_t)M * N * 2, 256) + qoq_linear_workspace_bytes(M, N, K);
+    return align_up(qoq_linear_workspace_bytes(M, N, K), 256) + align_up((size_t)M * K * 2, 256) + (size_t)M * N * 2;
 }
 
 int qoq_linear_host(const void* X_host, int M, int K, const void* packed, const void* s0, int N, void* Y_host,
@@ -218,9 +221,9 @@ int qoq_linear_host(const void* X_host, int M, int K, const void* packed, const 
     if (scratch_bytes < qoq_linear_host_scratch_bytes(M, N, K)) return QOQ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint8_t* b = static_cast<uint8_t*>(scratch);
+    void* ws = b;                b += align_up(qoq_linear_workspace_bytes(M, N, K), 256);
     void* Xd = b;                b += align_up((size_t)M * K * 2, 256);
-    void* Yd = b;                b += align_up((size_t)M * N * 2, 256);
-    void* ws = b;
+    void* Yd = b;
     if (cudaMemcpyAsync(Xd, X_host, (size_t)M * K * 2, cudaMemcpyHostToDevice, st) != cudaSuccess)
         return QOQ_ERR_CUDA;
     if ((rc = run_linear(Xd, K, M, N, K, 128, packed, s0, Yd, N, ws, qoq_linear_workspace_bytes(M, N, K), st)))

@@ -171,6 +171,36 @@ def test_linear_host_e2e(gpu_lib):
     check_y(Yh, oracle.linear_rows(X, p_ref, s0_ref, N))
 
 
+@pytest.mark.parametrize("M", [1, 64])
+def test_linear_host_shared_scratch_decode_shapes(gpu_lib, M):
+    """The bench's e2e pattern: one scratch shared by the Llama-3-8B decode projections, called in a
+    loop with H2D / D2H copies between launches. The sync words sit at offset 0 for every shape, so
+    a larger shape's X copy never lands on a smaller shape's handshake counters (regression: the
+    old [X][Y][workspace] layout moved the counters with K and faulted). Y must equal the two-call
+    path (quantizer + GEMM) bit for bit on every pass."""
+    shapes = [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)]
+    gen = torch.Generator(device=dev()).manual_seed(5)
+    packs, refs, hosts = [], [], []
+    nbytes = max(gpu_lib.linear_host_scratch_bytes(M, N, K) for N, K in shapes)
+    assert all(gpu_lib.gemm_workspace_bytes(M, N, K) == 0 for N, K in shapes)   # reuse rule holds
+    scratch = torch.zeros(nbytes, dtype=torch.uint8, device=dev())
+    for i, (N, K) in enumerate(shapes):
+        W = (torch.randn(N, K, generator=gen, device=dev()) / K ** 0.5).half()
+        p, s0 = gpu_lib.quantize_weights(W)
+        X = torch.randn(M, K, generator=gen, device=dev()).half()
+        qx, sx, tx = gpu_lib.quantize_activations_per_token(X)
+        refs.append(gpu_lib.w4a8_gemm(qx, sx, tx, p, s0, N).cpu())
+        packs.append((p, s0, N))
+        hosts.append((X.cpu().pin_memory(), torch.empty(M, N, dtype=torch.float16).pin_memory()))
+    for _ in range(3):
+        for (p, s0, N), (Xh, Yh), ref in zip(packs, hosts, refs):
+            Yh.zero_()
+            gpu_lib.linear_host(Xh, p, s0, N, Yh, scratch)
+            torch.cuda.synchronize()
+            assert torch.equal(Yh, ref)
+    assert int(scratch[:256].count_nonzero()) == 0
+
+
 @pytest.mark.parametrize("mode", ["0", "1", "2"])
 @pytest.mark.parametrize("M,N,K", [(16, 256, 256), (1, 1280, 1024), (64, 512, 2048), (33, 384, 1152),
                                    (64, 4096, 4096)])
@@ -309,13 +339,13 @@ def test_fused_linear_bit_exact(gpu_lib, monkeypatch, mode, M, N, K, ldx):
         torch.cuda.synchronize()
         assert torch.equal(Y, two), f"rep {rep}: fused Y differs from quantizer + GEMM"
         check_y(Y, y_ref)
-        qx, sx, tx = gpu_lib.linear_workspace_views(ws, M, K)
+        qx, sx, tx = gpu_lib.linear_workspace_views(ws, M, N, K)
         assert np.array_equal(qx.cpu().numpy(), qx_ref)
         assert np.array_equal(bits16(sx), sx_ref.view(np.uint16))
         assert np.array_equal(tx.cpu().numpy(), tx_ref)
         assert int(ws[:256].count_nonzero()) == 0, "handshake counters not re-zeroed"
-        o = 256 + (M * K + 255) // 256 * 256 + (2 * M + 255) // 256 * 256 + (4 * M + 255) // 256 * 256
-        assert int(ws[o:].count_nonzero()) == 0, "split-K workspace not restored"
+        o = 256 + (gpu_lib.gemm_workspace_bytes(M, N, K) + 255) // 256 * 256
+        assert int(ws[256:o].count_nonzero()) == 0, "split-K workspace not restored"
 
 
 def test_fused_linear_in_cuda_graph(gpu_lib):
