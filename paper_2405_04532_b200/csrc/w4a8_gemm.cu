@@ -34,7 +34,7 @@
 
 // Timing ablations (never in production builds; results are garbage when set):
 //   2: no activation TMA (xfull arrives without data)   4: no weight bulk copies (wfull arrives)
-//   8: dequant skips the ALU expansion
+//   8: dequant skips the ALU expansion   16: dequant skips the TMEM stores
 #ifndef QOQ_ABLATE
 #define QOQ_ABLATE 0
 #endif
@@ -79,14 +79,20 @@ struct Cfg {
     static constexpr int kActRows = BN / CG;                          // activation rows held by this CTA
     static constexpr int kActBytes = kActRows * 128;                  // one k-tile of this CTA's activations
     static constexpr int kXStageBytes = 2 * kActBytes;                // activations of one step (1024-aligned)
-    static constexpr int kChunk = BN < 32 ? BN : 32;                  // TMEM columns per epilogue tcgen05.ld
+#ifndef QOQ_CHUNK
+#define QOQ_CHUNK 32
+#endif
+    static constexpr int kChunk = BN < QOQ_CHUNK ? BN : QOQ_CHUNK;    // TMEM columns per epilogue tcgen05.ld
     static constexpr int kStgBytes = kChunk * 128 * 4;                // one INT32 staging buffer [kChunk][128]
     static constexpr int kEpiBytes = 2 * kStgBytes + BN * 8;          // 2 staging buffers + per-token s_x, 128 t_x
     static constexpr int kARot = kDeqGroups % 2 == 0 ? kDeqGroups : 2 * kDeqGroups;   // lcm(2, groups)
     // two accumulator stages if they leave room for at least one A-ring rotation (2 x 64 columns
     // per rotation unit), else one
-    static constexpr int kAccStages = ((512 - 2 * kIssuers * BN) / 64 >= (kARot > 4 ? kARot : 4)) ? 2 : 1;
-    static constexpr int kAccCols = kAccStages * kIssuers * BN;
+    // Both MMA issuers accumulate into ONE accumulator per stage (the tensor pipe applies their
+    // MMAs in order; integer sums are order-free), pre-zeroed by the epilogue warps, so the
+    // epilogue reads BN columns, not 2 BN (tcgen05.ld is ~64 B/cycle/SM: the epilogue's bound).
+    static constexpr int kAccStages = ((512 - 2 * BN) / 64 >= (kARot > 4 ? kARot : 4)) ? 2 : 1;
+    static constexpr int kAccCols = kAccStages * BN;
     // Three independent rings: W (packed weights, HBM-latency bound, SMEM), X (activation k-tiles,
     // L2-latency bound, SMEM) and A (expanded weights, 64 TMEM columns per step). (Loading weights
     // straight from L2 into registers after a bulk L2 prefetch was measured slower on B200: the
@@ -97,10 +103,11 @@ struct Cfg {
     static constexpr int kARaw0 = (512 - kAccCols) / 64;
     static constexpr int kARaw = kARaw0 > 6 ? 6 : kARaw0;
     static constexpr int kAStages = (kARaw / kARot) * kARot;
+    static constexpr int kXStagesDef = BN <= 32 ? (kDeqGroups == 3 ? 6 : 8) : BN == 64 ? 6 : 2;
 #ifndef QOQ_XSTAGES
-    static constexpr int kXStages = BN <= 32 ? (kDeqGroups == 3 ? 6 : 8) : BN == 64 ? 6 : 2;
+    static constexpr int kXStages = kXStagesDef;
 #else
-    static constexpr int kXStages = BN <= 64 ? QOQ_XSTAGES : 2;
+    static constexpr int kXStages = (BN <= 64 && CG == 1) ? QOQ_XSTAGES : kXStagesDef;
 #endif
     static constexpr int kWStageBytes = ((2 * kTileBytes + 1023) / 1024) * 1024;   // packed weights of one step
     static constexpr int kWRaw = (212 * 1024 - kEpiBytes - kXStages * kXStageBytes) / kWStageBytes;
@@ -380,6 +387,20 @@ __device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<
     else tmem_ld_32x32b_x16(taddr, v);
 }
 
+// Zero this warp's 32 TMEM lanes of a BN-column accumulator (tcgen05.st, then wait::st).
+template <int BN>
+__device__ __forceinline__ void zero_acc(uint32_t taddr) {
+    if constexpr (BN >= 32) {
+        const uint32_t z[32] = {0};
+#pragma unroll
+        for (int c = 0; c < BN; c += 32) tmem_st_32x32b_x32(taddr + c, z);
+    } else {
+        const uint32_t z[16] = {0};
+        tmem_st_32x32b_x16(taddr, z);
+    }
+    tmem_wait_st();
+}
+
 template <int BN, bool OUT_I32, int CG>
 __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
@@ -533,9 +554,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
         }
     } else if (warp == 1 || warp == C::R::kMma1Warp) {
         // ===================== MMA issuers (one thread each). Issuer j takes the steps of a segment
-        // with local index % kIssuers == j, accumulating into its own TMEM accumulator. It waits only
-        // on afull[x]: the dequant warps arrive there after acquiring xfull[x], so the TMA-written
-        // activation tile of slot x is visible through that release/acquire chain.
+        // with global index % kIssuers == j; both accumulate (accumulate = 1 always) into the stage's
+        // shared accumulator, which the epilogue zeroed before freeing it. It waits only on afull[x]:
+        // the dequant warps arrive there after acquiring xfull[x], so the TMA-written activation tile
+        // of slot x is visible through that release/acquire chain.
         const int j = (warp == 1) ? 0 : 1;
         if (j < C::kIssuers && rank == 0) {   // whole warp runs the loop (warp-uniform descriptors); one lane issues
             const uint32_t idesc = idesc_i8(128 * CG, BN, /*a_signed=*/p.tx == nullptr);
@@ -543,11 +565,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
             int tile, s0, s1, cst = 0, it0 = 0;
             uint32_t cph = 0;
             while (si.next(tile, s0, s1)) {
-                mbar_wait(&accempty[cst], cph ^ 1);
+                mbar_wait(&accempty[cst], cph);   // phase k: zeroed for its k-th use (epilogue)
                 tc_fence_after();
-                const uint32_t d = tmem + C::kAStages * 64 + (cst * C::kIssuers + j) * BN;
+                const uint32_t d = tmem + C::kAStages * 64 + cst * BN;
                 // issuer j takes the steps with GLOBAL index it % kIssuers == j (so each X slot / A
-                // buffer is always consumed by the same issuer); first own step zero-initializes
+                // buffer is always consumed by the same issuer)
                 const int first = (j - it0 % C::kIssuers + C::kIssuers) % C::kIssuers;
                 for (int local = first; local < s1 - s0; local += C::kIssuers) {
                     const int it = it0 + local, sg = s0 + local;
@@ -567,9 +589,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
                                 const uint64_t bdesc = smem_desc_sw128(sb + t * C::kActBytes + kk * 32);
-                                const uint32_t accum = (local > first || t > 0 || kk > 0) ? 1u : 0u;
-                                if constexpr (CG == 2) mma_i8_ts2(d, a + t * 32 + kk * 8, bdesc, idesc, accum);
-                                else mma_i8_ts(d, a + t * 32 + kk * 8, bdesc, idesc, accum);
+                                if constexpr (CG == 2) mma_i8_ts2(d, a + t * 32 + kk * 8, bdesc, idesc, 1u);
+                                else mma_i8_ts(d, a + t * 32 + kk * 8, bdesc, idesc, 1u);
                                 if (QOQ_TRACING && p.trace && blockIdx.x == 0 && it < 16)
                                     p.trace[kTrMma + it * 8 + t * 4 + kk] = clock64();
                             }
@@ -646,7 +667,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                             uint32_t out[32];
                             if (signed_a) expand_row<true>(v[t], sc[t], bias[t], out);
                             else expand_row<false>(v[t], sc[t], bias[t], out);
-                            tmem_st_32x32b_x32(tmem + lane_off + as * 64 + t * 32, out);
+                            if (!(QOQ_ABLATE & 16)) tmem_st_32x32b_x32(tmem + lane_off + as * 64 + t * 32, out);
+                            else if (out[0] == 0x12345678u && out[31] == 0x9abcdef0u) asm volatile("trap;");
                         }
                     }
                     tmem_wait_st();
@@ -670,6 +692,16 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
         const int et = threadIdx.x - C::R::kEpiThread0;   // 0..127 for cooperative phases
         const int g = et >> 5, l = et & 31;           // vector mapping: rows 4l..4l+3, tokens g, g+4, ...
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        // every accumulator stage starts zeroed: completes phase 0 of accempty (the issuers' first wait)
+        for (int st = 0; st < C::kAccStages; ++st) {
+            zero_acc<BN>(tmem + lane_off + C::kAStages * 64 + st * BN);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&accempty[st]), 0));
+                else mbar_arrive(&accempty[st]);
+            }
+        }
         pdl_wait();
         if (et == 0) QOQ_TRACE(p, 12);
         if (p.X) {   // fused per-token quantization of X, then the grid handshake (s_x / t_x below)
@@ -683,17 +715,13 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
             named_bar_sync(1, 128);
         }
         SegIter si(p, CG);
-        int tile, s0, s1, cst = 0, it0e = 0;
+        int tile, s0, s1, cst = 0;
         uint32_t cph = 0;
         while (si.next(tile, s0, s1)) {
             const int nt = (tile / p.MT) * CG + rank, mt = tile % p.MT;
             tile = nt * p.MT + mt;   // the real 128-row tile of this CTA (workspace / counters index)
             const int n0 = nt * 128, m0 = mt * BN;
-            // a 1-step segment lives in the accumulator of the issuer that owns that global step
-            const int single = (C::kIssuers == 2 && s1 - s0 == 1) ? (it0e % 2) : 0;
-            it0e += s1 - s0;
             const bool whole = (s0 == 0 && s1 == p.KS);
-            const bool two = (C::kIssuers == 2) && (s1 - s0 >= 2);   // second accumulator holds data
             int32_t* wst = p.ws + (size_t)tile * 128 * BN;
             for (int jj = et; jj < BN; jj += 128) {
                 const int m = m0 + jj;
@@ -712,7 +740,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
             mbar_wait(&accfull[cst], cph);
             if (et == 0) QOQ_TRACE(p, 6);
             tc_fence_after();
-            const uint32_t d = tmem + lane_off + C::kAStages * 64 + (cst * C::kIssuers + single) * BN;
+            const uint32_t d = tmem + lane_off + C::kAStages * 64 + cst * BN;
             if (clustered) {
                 // ---- cluster split-K, reduce-scatter through DSMEM: stage this CTA's partial (sum of
                 // both issuers' accumulators) row-major [128][BN+4] in its now-idle X ring; the rows
@@ -723,27 +751,33 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                     const int j0 = ci * C::kChunk;
                     uint32_t v[C::kChunk];
                     tmem_ld_chunk<BN>(d + j0, v);
-                    if (two) {
-                        uint32_t v2[C::kChunk];
-                        tmem_ld_chunk<BN>(d + BN + j0, v2);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < C::kChunk; ++i) v[i] += v2[i];
-                    } else {
-                        tmem_wait_ld();
-                    }
+                    tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < C::kChunk; i += 4)
                         *reinterpret_cast<int4*>(part + r * kRP + j0 + i) =
                             make_int4((int)v[i], (int)v[i + 1], (int)v[i + 2], (int)v[i + 3]);
                 }
+                zero_acc<BN>(d);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accempty[cst]);
                 fence_proxy_async_smem();
+                if (et == 0) QOQ_TRACE(p, 23);
                 named_bar_sync(1, 128);
+                if (et == 0) QOQ_TRACE(p, 24);
                 cluster_wait_acquire();   // every CTA's zeroed slice + armed red_full (setup arrive)
+                if (et == 0) QOQ_TRACE(p, 25);
                 const int R = 128 / p.S;
+                // this thread's output rows are the same 4 in every write-out iteration below
+                // (w % nq is invariant): fetch their s0 now, off the critical path
+                const int nq = R / 4;
+                float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                if constexpr (!OUT_I32) {
+                    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p.s0 + n0 + crank * R + (et % nq) * 4));
+                    const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+                    const float2 fa = __half22float2(h2[0]), fb = __half22float2(h2[1]);
+                    s4[0] = fa.x; s4[1] = fa.y; s4[2] = fb.x; s4[3] = fb.y;
+                }
                 if (et < p.S) {   // thread c sends slice c to cluster rank c
                     const uint32_t bytes = (uint32_t)(R * kRP * 4);
                     bulk_reduce_add_s32_cluster(mapa_shared(smem_u32(stg), et), part + et * R * kRP, bytes,
@@ -751,27 +785,40 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                 }
                 if (et == 0) QOQ_TRACE(p, 7);
                 mbar_wait(red_full, 0);
+                if (et == 0) QOQ_TRACE(p, 22);
                 // every slice this CTA receives has landed, so every read of the peers' partials that
                 // targets it is done: arrive on the exit barrier now and overlap its latency with
-                // the write-out below
-                cluster_arrive_release();
+                // the write-out below (relaxed: the barrier orders lifetimes, it publishes no data)
+                cluster_arrive_relaxed();
                 cl_done = true;
-                // this CTA's R rows, all BN tokens: thread -> (token jj, 4 consecutive rows)
-                const int nq = R / 4;
-                for (int w = et; w < nq * BN; w += 128) {
-                    const int jj = w / nq, rr = (w % nq) * 4;
-                    const int m = m0 + jj, n = n0 + crank * R + rr;
-                    if (m < p.M) {
-                        int4 a4 = make_int4(stg[(rr + 0) * kRP + jj], stg[(rr + 1) * kRP + jj],
-                                            stg[(rr + 2) * kRP + jj], stg[(rr + 3) * kRP + jj]);
-                        float s4[4] = {0.f, 0.f, 0.f, 0.f};
-                        if constexpr (!OUT_I32) {
-                            const uint2 u = __ldg(reinterpret_cast<const uint2*>(p.s0 + n));
-                            const __half2* h2 = reinterpret_cast<const __half2*>(&u);
-                            const float2 fa = __half22float2(h2[0]), fb = __half22float2(h2[1]);
-                            s4[0] = fa.x; s4[1] = fa.y; s4[2] = fb.x; s4[3] = fb.y;
+                // this CTA's R rows, all BN tokens: thread -> (token jj, 4 consecutive rows); w % nq
+                // is fixed per thread, so thread et covers tokens et / nq + (128 / nq) u. All
+                // shared-memory reads first, then the guarded stores (see the mode-0 write-out).
+                if constexpr (BN <= 64) {                       // mode 2 only runs BN <= 64 (plan_gemm)
+                    constexpr int kU = BN / 8;                   // iterations at the smallest slice (S = 2)
+                    constexpr int kB = kU < 4 ? kU : 4;          // batch (register budget)
+                    const int rr = (et % nq) * 4, n = n0 + crank * R + rr, step = 128 / nq;
+                    const int items = nq * BN;                   // item w = et + 128 u
+#pragma unroll 1
+                    for (int u0 = 0; u0 < kU && et + 128 * u0 < items; u0 += kB) {
+                        int4 av[kB];
+                        float sv[kB];
+                        int tv[kB];
+#pragma unroll
+                        for (int b = 0; b < kB; ++b) {
+                            const int u = u0 + b, jj = et / nq + step * u;
+                            if (et + 128 * u < items) {
+                                av[b] = make_int4(stg[(rr + 0) * kRP + jj], stg[(rr + 1) * kRP + jj],
+                                                  stg[(rr + 2) * kRP + jj], stg[(rr + 3) * kRP + jj]);
+                                sv[b] = sxs[jj];
+                                tv[b] = txs[jj];
+                            }
                         }
-                        write_out4<OUT_I32>(p, m, n, a4, txs[jj], sxs[jj], s4);
+#pragma unroll
+                        for (int b = 0; b < kB; ++b) {
+                            const int u = u0 + b, m = m0 + et / nq + step * u;
+                            if (et + 128 * u < items && m < p.M) write_out4<OUT_I32>(p, m, n, av[b], tv[b], sv[b], s4);
+                        }
                     }
                 }
                 if (et == 0) QOQ_TRACE(p, 9);
@@ -785,16 +832,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                 int32_t* sb = stg + (ci & 1) * (C::kChunk * 128);
                 uint32_t v[C::kChunk];
                 tmem_ld_chunk<BN>(d + j0, v);
-                if (two) {
-                    uint32_t v2[C::kChunk];
-                    tmem_ld_chunk<BN>(d + BN + j0, v2);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < C::kChunk; ++i) v[i] += v2[i];
-                } else {
-                    tmem_wait_ld();
-                }
-                if (ci == BN / C::kChunk - 1) {          // accumulators fully read: hand TMEM back
+                tmem_wait_ld();
+                if (et == 0 && ci == 0) QOQ_TRACE(p, 27);
+                if (ci == BN / C::kChunk - 1) {          // accumulator fully read: zero it, hand it back
+                    zero_acc<BN>(d);
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
@@ -802,10 +843,13 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                         else mbar_arrive(&accempty[cst]);
                     }
                 }
+                if (et == 0 && ci == 1) QOQ_TRACE(p, 30);
                 if (et == 0) bulk_wait_read<1>();        // staging buffer (ci & 1) no longer read by TMA
                 named_bar_sync(1, 128);
+                if (et == 0 && ci == 0) QOQ_TRACE(p, 28);
 #pragma unroll
                 for (int i = 0; i < C::kChunk; ++i) sb[i * 128 + r] = (int32_t)v[i];
+                if (et == 0 && ci == 0) QOQ_TRACE(p, 31);
                 if (!whole) {
                     fence_proxy_async_smem();
                     named_bar_sync(1, 128);
@@ -815,15 +859,29 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                     }
                 } else {
                     named_bar_sync(1, 128);
+                    // all shared-memory reads first, then the stores: the (m < M) guards would
+                    // otherwise serialize one LDS -> convert -> STG latency chain per token
+                    constexpr int kU = C::kChunk / 4;
+                    int4 av[kU];
+                    float sv[kU];
+                    int tv[kU];
 #pragma unroll
-                    for (int jj = g; jj < C::kChunk; jj += 4) {
-                        const int m = m0 + j0 + jj;
-                        if (m < p.M)
-                            write_out4<OUT_I32>(p, m, n0 + 4 * l, *reinterpret_cast<const int4*>(sb + jj * 128 + 4 * l),
-                                                txs[j0 + jj], sxs[j0 + jj], s0v);
+                    for (int u = 0; u < kU; ++u) {
+                        const int jj = g + 4 * u;
+                        av[u] = *reinterpret_cast<const int4*>(sb + jj * 128 + 4 * l);
+                        sv[u] = sxs[j0 + jj];
+                        tv[u] = txs[j0 + jj];
                     }
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const int m = m0 + j0 + g + 4 * u;
+                        if (m < p.M && !(QOQ_ABLATE & 32)) write_out4<OUT_I32>(p, m, n0 + 4 * l, av[u], tv[u], sv[u], s0v);
+                        else if ((QOQ_ABLATE & 32) && av[u].x == 0x7fffffff && sv[u] == 1.2345f) asm volatile("trap;");
+                    }
+                    if (et == 0 && ci == 0) QOQ_TRACE(p, 29);
                 }
             }
+            if (et == 0) QOQ_TRACE(p, 26);
             if (++cst == C::kAccStages) { cst = 0; cph ^= 1; }
             if (!whole) {
                 if (et == 0) {
@@ -864,6 +922,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
 
     tc_fence_before();
     if (threadIdx.x == C::R::kEpiThread0) QOQ_TRACE(p, 14);
+    // mode 2: the exit barrier (phase 1) must only wait for every CTA's slices to land (the epilogue
+    // threads arrive right after red_full); threads that never touch peer memory arrive as soon as
+    // their role is done, not after this CTA's write-out.
+    if (clustered && !cl_done) {
+        cluster_wait_acquire();
+        cluster_arrive_relaxed();
+        cl_done = true;
+    }
     __syncthreads();
     if (threadIdx.x == 0) QOQ_TRACE(p, 15);
     // mode 2: no CTA may exit while a peer's bulk reduce still reads its partial or writes its slice:
@@ -872,10 +938,6 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
     if (CG == 2) {
         cluster_sync_all();
     } else if (clustered) {
-        if (!cl_done) {
-            cluster_wait_acquire();
-            cluster_arrive_release();
-        }
         cluster_wait_acquire();
     }
     if (threadIdx.x == 0) QOQ_TRACE(p, 10);

@@ -24,7 +24,8 @@ import synth  # noqa: E402
 
 NAMES = ["start", "setup", "prod_pdl", "quant_rows", "handshake", "mma_done", "epi_acc", "epi_red", "seg_done",
          "finalized", "end", "mbar_init", "epi_pdl", "sync0", "epi_exit", "sync_end",
-         "q_loaded", "q_scale", "q_stored", "q_row_done", "q_all_rows", "q_fence"]
+         "q_loaded", "q_scale", "q_stored", "q_row_done", "q_all_rows", "q_fence",
+         "red_landed", "part_staged", "part_bar", "cl_acq", "epi_chunks", "epi_ld0", "epi_sts0", "epi_stg0", "epi_ld1", "epi_sts_done"]
 EV = 32
 IT = 148 * EV
 CYC = IT + 64 * 8 + 16 * 8 * 2
