@@ -16,6 +16,7 @@ constexpr int kTileBytes = 8448;     // 8192 B of u4 codes + 128 B s_u8 + 128 B 
 struct GemmPlan {
     int BN;          // token tile = MMA N (16, 32, 64, 128 or 256)
     int MT, NT, KT;  // token tiles, 128-row weight tiles, 128-deep K tiles
+    int MB;          // token tiles per band of the work order (tile_coords in w4a8_gemm.cu)
     int KS;          // pipeline steps per output tile (2 k-tiles each, last may hold 1)
     int T;           // output tiles = MT * NT
     long long I;     // steps = T * KS

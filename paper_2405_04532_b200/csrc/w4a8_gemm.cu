@@ -75,7 +75,10 @@ struct Cfg {
     static constexpr int kDeqGroups = (BN <= 64) ? QOQ_DEQ_GROUPS : 2;
     using R = Roles<kDeqGroups>;
     static constexpr int kBlockThreads = R::kBlockThreads;
-    static constexpr int kIssuers = BN <= 128 ? 2 : 1;
+#ifndef QOQ_ISSUERS_BIG
+#define QOQ_ISSUERS_BIG 2
+#endif
+    static constexpr int kIssuers = BN <= 128 ? 2 : QOQ_ISSUERS_BIG;
     static constexpr int kActRows = BN / CG;                          // activation rows held by this CTA
     static constexpr int kActBytes = kActRows * 128;                  // one k-tile of this CTA's activations
     static constexpr int kXStageBytes = 2 * kActBytes;                // activations of one step (1024-aligned)
@@ -91,7 +94,10 @@ struct Cfg {
     // Both MMA issuers accumulate into ONE accumulator per stage (the tensor pipe applies their
     // MMAs in order; integer sums are order-free), pre-zeroed by the epilogue warps, so the
     // epilogue reads BN columns, not 2 BN (tcgen05.ld is ~64 B/cycle/SM: the epilogue's bound).
-    static constexpr int kAccStages = ((512 - 2 * BN) / 64 >= (kARot > 4 ? kARot : 4)) ? 2 : 1;
+    // (BN = 192: 2 x 192 accumulator columns + a 2-step A ring fill TMEM exactly, so the epilogue of
+    // one prefill tile overlaps the next tile's mainloop)
+    static constexpr int kAccStages =
+        ((512 - 2 * BN) / 64 >= (BN > 128 ? kARot : kARot > 4 ? kARot : 4)) ? 2 : 1;
     static constexpr int kAccCols = kAccStages * BN;
     // Three independent rings: W (packed weights, HBM-latency bound, SMEM), X (activation k-tiles,
     // L2-latency bound, SMEM) and A (expanded weights, 64 TMEM columns per step). (Loading weights
@@ -140,6 +146,7 @@ struct KParams {
     int32_t* ws;
     int* counters;
     int M, MT, KT, KS, T, G, mode, S;   // mode 2: S-CTA clusters split one tile's K range
+    int MB;                      // token tiles per band of the work order (tile_coords)
     long long I;                 // total steps = T * KS
     unsigned long long* trace;   // debug: per-CTA %globaltimer stamps (nullptr in production)
     // fused per-token activation quantization (qoq_w4a8_linear, M <= 64): X != nullptr. The
@@ -185,6 +192,19 @@ constexpr int kTraceCyc = kTrDq + 16 * 8;
 #define QOQ_TRACE(p, ev) do { } while (0)
 #define QOQ_TRACE_IT(p, it, ev) do { } while (0)
 #endif
+
+// Work unit t -> (n unit, token tile). Band-major: bands of MB token tiles; inside a band the n unit
+// is major and the token tile minor, so the CTAs of one wave share each weight tile (L2) and keep
+// re-reading one band of activations (MB x BN x K bytes, sized to stay in L2) instead of all of
+// them — long-K prefill (down_proj) would otherwise re-stream q_x from HBM every wave. MB = MT is
+// the plain token-tile-minor order (decode: MT = 1).
+__device__ __forceinline__ void tile_coords(const KParams& p, int t, int& nu, int& mt) {
+    const int nun = p.T / p.MT;                  // n units (128-row tiles, or tile pairs for CG = 2)
+    const int band = t / (p.MB * nun), r = t - band * (p.MB * nun);
+    const int mb = min(p.MB, p.MT - band * p.MB);
+    nu = r / mb;
+    mt = band * p.MB + (r - nu * mb);
+}
 
 // Iterates the (tile, s0, s1) segments (ranges of steps of one output tile) a CTA owns.
 // Every role runs an identical copy.
@@ -239,7 +259,9 @@ struct WProducer {
         int tile, s0;
         live = si.next(tile, s0, s1);
         sg = s0;
-        nt = live ? (tile / p.MT) * cg + rank : 0;
+        int nu = 0, mt;
+        if (live) tile_coords(p, tile, nu, mt);
+        nt = nu * cg + rank;
         pol = policy_evict_first();   // each weight byte is read once
     }
     __device__ bool issue(const KParams& p, uint8_t* smem, uint64_t* wfull, uint64_t* wfree) {
@@ -258,7 +280,11 @@ struct WProducer {
             int tile, s0;
             live = si.next(tile, s0, s1);
             sg = s0;
-            if (live) nt = (tile / p.MT) * cg + rank;
+            if (live) {
+                int nu, mt;
+                tile_coords(p, tile, nu, mt);
+                nt = nu * cg + rank;
+            }
         }
         return true;
     }
@@ -534,7 +560,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
             int tile, s0, s1, xs = 0, it = 0;
             uint32_t xph = 0;
             while (si.next(tile, s0, s1)) {
-                const int mt = tile % p.MT;
+                int nu, mt;
+                tile_coords(p, tile, nu, mt);
                 const int row0 = mt * BN + rank * C::kActRows;   // CG = 2: this CTA's half of the tokens
                 for (int sg = s0; sg < s1; ++sg, ++it) {
                     const int kt0 = 2 * sg, nk = (kt0 + 1 < p.KT) ? 2 : 1;
@@ -718,7 +745,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
         int tile, s0, s1, cst = 0;
         uint32_t cph = 0;
         while (si.next(tile, s0, s1)) {
-            const int nt = (tile / p.MT) * CG + rank, mt = tile % p.MT;
+            int nu, mt;
+            tile_coords(p, tile, nu, mt);
+            const int nt = nu * CG + rank;
             tile = nt * p.MT + mt;   // the real 128-row tile of this CTA (workspace / counters index)
             const int n0 = nt * 128, m0 = mt * BN;
             const bool whole = (s0 == 0 && s1 == p.KS);
@@ -1003,8 +1032,37 @@ static int max_clusters_bn(int BN, int S) {
 
 GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     GemmPlan p{};
-    p.BN = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+    // token tile: the smallest of 16/32/64/128 that holds M; above that 192 (double-buffered TMEM
+    // accumulators: the epilogue overlaps the next tile) except 192 < M <= 256, one 256-wide tile.
+    // QOQ_BN_BIG=256 forces the single-buffered 256-wide tile above M = 128 (A/B).
+    p.BN = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
+    if (M > 128) {
+        // prefill: pick the token tile by whole waves x per-tile cost, among tiles that fill the GPU
+        // (T >= #SMs: mode 0; below that the stream-K partials of wide tiles cost more than they
+        // save). Relative per-token costs measured on B200 (tools/prefill_ab.sh): BN = 128 expands
+        // each weight tile for half as many tokens (~1.2x); BN = 256 runs its epilogue without
+        // overlap (~1.2x at K = 4096, shrinking with K). QOQ_BN_BIG=128/192/256 forces.
+        const char* fb = getenv("QOQ_BN_BIG");
+        const int force = fb ? atoi(fb) : 0;
+        const int cand[3] = {128, 192, 256};
+        const double eff[3] = {1.2, 1.0, 1.0 + 0.2 * 4096.0 / K};
+        double best = 1e300;
+        p.BN = 128;
+        for (int i = 0; i < 3; ++i) {
+            const long long mt = (M + cand[i] - 1) / cand[i], t = mt * (N / kTileN);
+            const double cost = (double)((t + num_sms - 1) / num_sms) * cand[i] * eff[i];
+            if (force ? force == cand[i] : (t >= num_sms && cost < best)) {
+                best = cost;
+                p.BN = cand[i];
+            }
+        }
+    }
     p.MT = (M + p.BN - 1) / p.BN;
+    {   // activation band of the work order: <= 32 MB of q_x (tile_coords)
+        const long long per = (long long)p.BN * K;
+        const long long mb = (32ll << 20) / (per > 0 ? per : 1);
+        p.MB = (int)(mb < 1 ? 1 : mb > p.MT ? p.MT : mb);
+    }
     p.NT = N / kTileN;
     p.KT = K / kTileK;
     p.T = p.MT * p.NT;
@@ -1058,7 +1116,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     // tile pairs: T = units, G = pairs (the grid is 2G CTAs in clusters of 2).
     const char* fp = getenv("QOQ_FORCE_CG");
     const int force_cg = fp ? atoi(fp) : -1;
-    const bool pair_ok = p.mode != 2 && p.NT % 2 == 0 && p.BN >= 32;
+    const bool pair_ok = p.mode != 2 && p.NT % 2 == 0 && p.BN >= 32 && p.BN != 192;
     // Opt-in for now (QOQ_FORCE_CG=2): bit-exact, but on B200 two of the four dequant warps' tcgen05.st
     // stall for thousands of cycles while the pair's cta_group::2 MMAs run (tools/trace_gemm.py), so
     // the pair pipeline is slower than single CTAs at decode sizes. See DESIGN.md §6.
@@ -1102,6 +1160,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
                        : nullptr;
     kp.M = a.M;
     kp.MT = pl.MT;
+    kp.MB = pl.MB;
     kp.KT = pl.KT;
     kp.KS = pl.KS;
     kp.T = pl.T;
@@ -1142,7 +1201,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
 template <int BN>
 static cudaError_t launch_bn_cg(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl) {
     if (p.CG == 2) {
-        if constexpr (BN >= 32)
+        if constexpr (BN >= 32 && BN != 192)
             return a.out_i32 ? launch_bn<BN, true, 2>(a, p, st, pdl) : launch_bn<BN, false, 2>(a, p, st, pdl);
         return cudaErrorInvalidValue;
     }
@@ -1155,6 +1214,7 @@ cudaError_t launch_w4a8_gemm(const GemmArgs& a, const GemmPlan& p, cudaStream_t 
         case 32: return launch_bn_cg<32>(a, p, st, pdl);
         case 64: return launch_bn_cg<64>(a, p, st, pdl);
         case 128: return launch_bn_cg<128>(a, p, st, pdl);
+        case 192: return launch_bn_cg<192>(a, p, st, pdl);
         case 256: return launch_bn_cg<256>(a, p, st, pdl);
         default: return cudaErrorInvalidValue;
     }
