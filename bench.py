@@ -311,6 +311,8 @@ def main():
     lws = qoq.Workspace(dev)     # linear workspace (also holds the call's q_x / s_x / t_x)
     lws.get(max(qoq.linear_workspace_bytes(M, N, K) for _, N, K, _, _ in shapes))
     fused_quant = args.fused_quant
+    if fused_quant:
+        os.environ["QOQ_LINEAR_FUSED"] = "1"   # w4a8_linear's opt-in one-kernel path (read per call)
 
     def run_step(gemm_only=False):
         n_launch = 0
@@ -435,56 +437,82 @@ def main():
     return 0
 
 
-def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes):
+def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes, nstreams=2):
+    """End to end through the C ABI (qoq_linear_host: pinned host X -> device -> w4a8_linear ->
+    pinned host Y) for every GEMM of the step. Consecutive calls alternate over `nstreams` CUDA
+    streams (each with its own scratch and host buffers), so one call's D2H copy overlaps the next
+    call's H2D copy and kernels (PCIe is full duplex); every copy of the step stays in the timed
+    region."""
     M = args.M
     gen = torch.Generator().manual_seed(3)
-    Xh = {}
-    Yh = {}
-    for name, N, K, kind, qg in shapes:
-        Xh[name] = (torch.randn(M, K, generator=gen) * 1.0).half().pin_memory()
-        Yh[name] = torch.empty(M, N, dtype=torch.float16).pin_memory()
-    # one scratch per projection shape (the header's workspace-reuse rule), shared by all layers
-    scratch = {name: torch.zeros(qoq.linear_host_scratch_bytes(M, N, K), dtype=torch.uint8, device=dev)
-               for name, N, K, _, _ in shapes}
+    streams = [stream] + [torch.cuda.Stream(dev) for _ in range(nstreams - 1)]
+    Xh, Yh, scratch, red = {}, {}, {}, {}
+    for j in range(nstreams):
+        for name, N, K, kind, qg in shapes:
+            Xh[j, name] = (torch.randn(M, K, generator=gen) * 1.0).half().pin_memory()
+            Yh[j, name] = torch.empty(M, N, dtype=torch.float16).pin_memory()
+            # one scratch per (stream, projection shape): the header's workspace-reuse rule
+            scratch[j, name] = torch.zeros(qoq.linear_host_scratch_bytes(M, N, K), dtype=torch.uint8, device=dev)
+            if kind == "row":
+                red[j, name] = torch.empty(M, N, dtype=torch.float16, device=dev)
     h2d = sum(M * K * 2 for _, N, K, _, _ in shapes) * layers
     d2h = sum(M * N * 2 for _, N, K, _, _ in shapes) * layers
-    red = {name: torch.empty(M, N, dtype=torch.float16, device=dev)
-           for name, N, K, kind, qg in shapes if kind == "row"}
 
     def one_step():
+        c = 0
         for l in range(layers):
             for i, (name, N, K, kind, qg) in enumerate(shapes):
+                j = c % nstreams
+                c += 1
+                st = streams[j]
                 p, s0 = packed[l][i]
-                qoq.linear_host(Xh[name], p, s0, N, Yh[name], scratch[name], stream=stream)
+                qoq.linear_host(Xh[j, name], p, s0, N, Yh[j, name], scratch[j, name], stream=st)
                 if kind == "row" and world > 1:
-                    with torch.cuda.stream(stream):
-                        red[name].copy_(Yh[name], non_blocking=True)
-                        dist.all_reduce(red[name])
-                        Yh[name].copy_(red[name], non_blocking=True)
+                    with torch.cuda.stream(st):
+                        red[j, name].copy_(Yh[j, name], non_blocking=True)
+                        dist.all_reduce(red[j, name])
+                        Yh[j, name].copy_(red[j, name], non_blocking=True)
+
+    def forked_step():
+        """one_step with the side streams forked from / joined into streams[0] (graph capture)."""
+        ev0 = torch.cuda.Event()
+        ev0.record(streams[0])
+        for st in streams[1:]:
+            st.wait_event(ev0)
+        one_step()
+        for st in streams[1:]:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            streams[0].wait_event(ev)
 
     steps = max(3, args.steps // 10)
-    with torch.cuda.stream(stream):
-        for _ in range(2):
-            one_step()
-        stream.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+    for _ in range(2):
+        forked_step()
+    torch.cuda.synchronize(dev)
+    # the step's API calls (copies + kernels of all 4 x layers linear_host calls) captured once as a
+    # CUDA graph and replayed: no per-call host overhead in the timed region, every copy still in it
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=streams[0]):
+        forked_step()
+    g.replay()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(streams[0]):
+        e0.record(streams[0])
         for _ in range(steps):
-            one_step()
-        e1.record(stream)
-        stream.synchronize()
+            g.replay()
+        e1.record(streams[0])
+    torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        h2d_rank, d2h_rank = h2d, d2h
-    else:
-        h2d_rank, d2h_rank = h2d, d2h
-    return {"value": step_bytes / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d_rank * world,
-            "d2h_bytes_per_step": d2h_rank * world, "ms_per_step": ms, "steps": steps,
-            "api": "qoq_linear_host (C ABI, pinned host X/Y) per GEMM"}
+    return {"value": step_bytes / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+            "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": steps, "streams": nstreams,
+            "api": "qoq_linear_host (C ABI, pinned host X/Y) per GEMM, calls alternating over "
+                   f"{nstreams} streams, the step captured as one CUDA graph"}
 
 
 def prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream):

@@ -106,10 +106,11 @@ int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed,
 /* The W4A8 linear layer on fp16 activations: per-token INT8 quantization of X (exactly
  * qoq_quantize_activations_per_token) followed by the W4A8 GEMM (exactly qoq_w4a8_gemm), so
  *   Y = qoq_w4a8_gemm(quantize(X))  bit for bit.
- * For M <= 64 (decode) both run in ONE kernel: the GEMM's epilogue warps quantize rows
- * m ≡ cta (mod grid) into the workspace while the weight stream is already in flight, and a grid
- * handshake in the workspace releases the activation loads; above 64 it launches the quantizer
- * kernel and then the GEMM.
+ * By default it launches the quantizer kernel and then the GEMM (PDL-chained). With the
+ * environment variable QOQ_LINEAR_FUSED=1 and M <= 64 both run in ONE kernel instead: the GEMM's
+ * epilogue warps quantize rows m ≡ cta (mod grid) into the workspace while the weight stream is
+ * already in flight, and a grid handshake in the workspace releases the activation loads
+ * (measured slower on B200 than the two-kernel chain, hence opt-in).
  *   X_fp16 [M][ldx] (ldx >= K, ldx % 8 == 0, 16-byte aligned).  packed / s0_fp16 from
  *   qoq_quantize_weights.  Y_fp16 [M][ldy], ldy >= N, ldy % 4 == 0.
  * workspace: qoq_linear_workspace_bytes(M,N,K) bytes, 256-byte aligned, ZERO-FILLED before first
@@ -140,7 +141,8 @@ int qoq_linear_host(const void* X_host_fp16, int M, int K,
 
 /* Kernels launched per successful call (launch accounting for benchmarks):
  * quantize_weights 2, quantize_activations_per_token 1, w4a8_gemm 1, w4a8_gemm_i32 1,
- * w4a8_linear 1 (M <= 64) or 2, linear_host as w4a8_linear (plus 2 async copies). */
+ * w4a8_linear 2 (1 when fused: QOQ_LINEAR_FUSED=1 and M <= 64), linear_host as w4a8_linear
+ * (plus 2 async copies). */
 
 #ifdef __cplusplus
 }

@@ -27,12 +27,17 @@ ABI_VERSION = 2
 # kernels launched per call (matches include/qoq_b200.h)
 LAUNCHES = {"quantize_weights": 2, "quantize_activations_per_token": 1, "w4a8_gemm": 1,
             "w4a8_gemm_i32": 1}
-FUSE_MAX_M = 64   # w4a8_linear / linear_host: one fused kernel up to this M, quantizer + GEMM above
+FUSE_MAX_M = 64   # w4a8_linear / linear_host with QOQ_LINEAR_FUSED=1: one fused kernel up to this M
+
+
+def linear_fused(M: int) -> bool:
+    """True when w4a8_linear runs the one-kernel fused path (opt-in: QOQ_LINEAR_FUSED=1, M <= 64)."""
+    return M <= FUSE_MAX_M and os.environ.get("QOQ_LINEAR_FUSED") == "1"
 
 
 def linear_launches(M: int) -> int:
     """Kernels one w4a8_linear (or linear_host) call launches."""
-    return 1 if M <= FUSE_MAX_M else 2
+    return 1 if linear_fused(M) else 2
 
 _lock = threading.Lock()
 _lib = None

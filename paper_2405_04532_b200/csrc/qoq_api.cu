@@ -3,6 +3,7 @@
 // point is cached in w4a8_gemm.cu).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/qoq_b200.h"
 #include "qoq_internal.h"
@@ -95,7 +96,12 @@ int run_linear(const void* X, int ldx, int M, int N, int K, int group, const voi
     if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return QOQ_ERR_INVALID_ARG;
     LinearWs w = linear_ws_layout(ws, M, N, K);
     if (ws_bytes < w.total) return QOQ_ERR_WORKSPACE;
-    if (M > kFuseMaxM) {
+    // Default: quantizer kernel + GEMM, PDL-chained (measured faster on B200 at every decode M: the
+    // fused kernel's grid-wide handshake costs more than the kernel boundary it removes).
+    // QOQ_LINEAR_FUSED=1 selects the one-kernel path for M <= kFuseMaxM.
+    const char* ff = getenv("QOQ_LINEAR_FUSED");
+    const bool fused = ff && atoi(ff) == 1;
+    if (M > kFuseMaxM || !fused) {
         if ((rc = qoq_quantize_activations_per_token(X, M, K, ldx, w.qx, w.sx, w.tx, st))) return rc;
         return run_gemm(w.qx, w.sx, w.tx, packed, s0, M, N, K, group, Y, ldy, false, w.gemm_ws, w.gemm_ws_bytes,
                         st);

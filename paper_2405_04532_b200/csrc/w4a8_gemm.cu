@@ -88,7 +88,15 @@ struct Cfg {
     static constexpr int kChunk = BN < QOQ_CHUNK ? BN : QOQ_CHUNK;    // TMEM columns per epilogue tcgen05.ld
     static constexpr int kStgBytes = kChunk * 128 * 4;                // one INT32 staging buffer [kChunk][128]
     static constexpr int kEpiBytes = 2 * kStgBytes + BN * 8;          // 2 staging buffers + per-token s_x, 128 t_x
-    static constexpr int kARot = kDeqGroups % 2 == 0 ? kDeqGroups : 2 * kDeqGroups;   // lcm(2, groups)
+    // QOQ_DEQ_SPLIT=1 (BN >= 128): the dequant groups split each step (group g expands k-tile g of
+    // every step) instead of taking alternate steps. Measured on B200 prefill: 1-3% slower (the
+    // step is bound by shared-memory bandwidth, not dequant latency), so off by default.
+#ifndef QOQ_DEQ_SPLIT
+#define QOQ_DEQ_SPLIT 0
+#endif
+    static constexpr bool kDeqSplit = QOQ_DEQ_SPLIT && BN >= 128 && kDeqGroups == 2;
+    static constexpr int kDeqRot = kDeqSplit ? 1 : kDeqGroups;                // dequant roles per ring slot
+    static constexpr int kARot = kDeqRot % 2 == 0 ? kDeqRot : 2 * kDeqRot;   // lcm(2 issuers, dequant roles)
     // two accumulator stages if they leave room for at least one A-ring rotation (2 x 64 columns
     // per rotation unit), else one
     // Both MMA issuers accumulate into ONE accumulator per stage (the tensor pipe applies their
@@ -118,7 +126,7 @@ struct Cfg {
     static constexpr int kWStageBytes = ((2 * kTileBytes + 1023) / 1024) * 1024;   // packed weights of one step
     static constexpr int kWRaw = (212 * 1024 - kEpiBytes - kXStages * kXStageBytes) / kWStageBytes;
     static constexpr int kWCap = kWRaw > 12 ? 12 : kWRaw;
-    static constexpr int kWStages = (kWCap / kDeqGroups) * kDeqGroups;
+    static constexpr int kWStages = (kWCap / kDeqRot) * kDeqRot;
     static constexpr int kColsUsed = kAStages * 64 + kAccCols;
     static constexpr int kTmemCols = kColsUsed <= 32 ? 32 : kColsUsed <= 64 ? 64 : kColsUsed <= 128 ? 128
                                    : kColsUsed <= 256 ? 256 : 512;
@@ -130,8 +138,8 @@ struct Cfg {
     static constexpr int kSmemBytes = 1024 + kBarOff + kBarBytes;
     static constexpr int kFinU = BN / 4 < 8 ? BN / 4 : 8;             // independent 16-B loads per finalize batch
     static_assert(kXStages >= 2 && kWStages >= 2 && kAStages >= 2, "pipeline too shallow");
-    static_assert(kXStages % kIssuers == 0 && kWStages % kDeqGroups == 0 && kAStages % kARot == 0, "ring rotation");
-    static_assert(CG == 1 || kXStages % kDeqGroups == 0, "ring rotation (pairs: dequant groups wait on X)");
+    static_assert(kXStages % kIssuers == 0 && kWStages % kDeqRot == 0 && kAStages % kARot == 0, "ring rotation");
+    static_assert(CG == 1 || kXStages % kDeqRot == 0, "ring rotation (pairs: dequant groups wait on X)");
     static_assert(kColsUsed <= 512, "TMEM overflow");
     static_assert(kSmemBytes <= 227 * 1024, "SMEM overflow");
 };
@@ -479,14 +487,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < C::kWStages; ++i) {
             mbar_init(&wfull[i], 1);
-            mbar_init(&wfree[i], 4);
+            mbar_init(&wfree[i], 4 * (C::kDeqSplit ? C::kDeqGroups : 1));
         }
         for (int i = 0; i < C::kXStages; ++i) {
             mbar_init(&xfull[i], 1);
             mbar_init(&xempty[i], 1);
         }
         for (int i = 0; i < C::kAStages; ++i) {
-            mbar_init(&afull[i], 4 * CG);     // CG = 2: the peer's dequant warps arrive remotely on the leader's
+            mbar_init(&afull[i], 4 * CG * (C::kDeqSplit ? C::kDeqGroups : 1));     // CG = 2: the peer's dequant warps arrive remotely on the leader's
             mbar_init(&aempty[i], 1);
         }
         for (int i = 0; i < C::kAccStages; ++i) {
@@ -646,8 +654,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
         }
     } else if (warp >= 2 && warp < C::R::kDeqWarp1) {
         // ===================== dequant: u4 -> (q̂ + 128) lanes -> TMEM buffer of the step's X slot
-        // Two 4-warp groups take alternate steps; in a group, warp (w & 3) owns TMEM lanes
-        // 32(w&3)..+31 and thread r expands weight row r of each k-tile (32 TMEM columns per tile).
+        // The 4-warp groups take alternate steps (kDeqSplit: group g expands k-tile g of every step);
+        // in a group, warp (w & 3) owns TMEM lanes 32(w&3)..+31 and thread r expands weight row r of
+        // each k-tile (32 TMEM columns per tile).
         const int q = warp & 3;                       // TMEM lane quarter this warp may access
         const int grp = (warp - 2) >> 2;              // steps it with it % kDeqGroups == grp
         const int r = q * 32 + lane;                  // weight row within the tile
@@ -659,7 +668,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
         uint32_t wph = 0;
         while (si.next(tile, s0, s1)) {
             for (int sg = s0; sg < s1; ++sg, ++it) {
-                if (it % C::kDeqGroups == grp) {
+                if (C::kDeqSplit || it % C::kDeqGroups == grp) {
                     const int nk = (2 * sg + 1 < p.KT) ? 2 : 1;
                     mbar_wait(&wfull[ws], wph);
                     if (tw) QOQ_TRACE_IT(p, it, 0);
@@ -668,7 +677,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                     uint32_t sc[2], bias[2];
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
-                        if (t < nk) {
+                        if (t < nk && (!C::kDeqSplit || t == grp)) {
                             const uint8_t* w = wb + t * kTileBytes;
                             sc[t] = w[8192 + r];
                             bias[t] = (128u - (uint32_t)w[8320 + r]) * 0x01010101u;
@@ -690,7 +699,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                     tc_fence_after();
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
-                        if (t < nk) {
+                        if (t < nk && (!C::kDeqSplit || t == grp)) {
                             uint32_t out[32];
                             if (signed_a) expand_row<true>(v[t], sc[t], bias[t], out);
                             else expand_row<false>(v[t], sc[t], bias[t], out);
@@ -1116,7 +1125,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     // tile pairs: T = units, G = pairs (the grid is 2G CTAs in clusters of 2).
     const char* fp = getenv("QOQ_FORCE_CG");
     const int force_cg = fp ? atoi(fp) : -1;
-    const bool pair_ok = p.mode != 2 && p.NT % 2 == 0 && p.BN >= 32 && p.BN != 192;
+    const bool pair_ok = p.mode != 2 && p.NT % 2 == 0 && p.BN >= 32;
     // Opt-in for now (QOQ_FORCE_CG=2): bit-exact, but on B200 two of the four dequant warps' tcgen05.st
     // stall for thousands of cycles while the pair's cta_group::2 MMAs run (tools/trace_gemm.py), so
     // the pair pipeline is slower than single CTAs at decode sizes. See DESIGN.md §6.
@@ -1201,7 +1210,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
 template <int BN>
 static cudaError_t launch_bn_cg(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl) {
     if (p.CG == 2) {
-        if constexpr (BN >= 32 && BN != 192)
+        if constexpr (BN >= 32)
             return a.out_i32 ? launch_bn<BN, true, 2>(a, p, st, pdl) : launch_bn<BN, false, 2>(a, p, st, pdl);
         return cudaErrorInvalidValue;
     }

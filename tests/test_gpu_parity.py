@@ -312,13 +312,21 @@ def _fused_case(M, N, K, ldx, seed):
     return X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref
 
 
+@pytest.mark.parametrize("path", ["fused", "two"])
 @pytest.mark.parametrize("mode", ["auto", "0", "1", "2", "cg2"])
 @pytest.mark.parametrize("M,N,K,ldx", FUSED_SHAPES)
-def test_fused_linear_bit_exact(gpu_lib, monkeypatch, mode, M, N, K, ldx):
-    """qoq_w4a8_linear (per-token quantization fused into the GEMM for M <= 64): the quantized
-    activations it leaves in the workspace equal the oracle's bit for bit, Y is bit-identical to the
-    two-call path (quantizer + GEMM) and within tolerance of the oracle, and repeated launches on
-    the same workspace (grid-handshake counters re-zeroed by the last CTA) stay exact."""
+def test_fused_linear_bit_exact(gpu_lib, monkeypatch, path, mode, M, N, K, ldx):
+    """qoq_w4a8_linear, on the fused path (QOQ_LINEAR_FUSED=1: per-token quantization inside the
+    GEMM for M <= 64) and on the default quantizer + GEMM chain: the quantized activations it leaves
+    in the workspace equal the oracle's bit for bit, Y is bit-identical to the two-call path
+    (quantizer + GEMM) and within tolerance of the oracle, and repeated launches on the same
+    workspace (grid-handshake counters re-zeroed by the last CTA) stay exact."""
+    if path == "fused":
+        monkeypatch.setenv("QOQ_LINEAR_FUSED", "1")
+    else:
+        monkeypatch.delenv("QOQ_LINEAR_FUSED", raising=False)
+    if path == "two" and mode not in ("auto", "2"):
+        pytest.skip("the two-kernel path is covered by the GEMM parity tests; auto/2 suffice here")
     if mode == "cg2":
         monkeypatch.setenv("QOQ_FORCE_CG", "2")
     elif mode != "auto":
@@ -348,9 +356,15 @@ def test_fused_linear_bit_exact(gpu_lib, monkeypatch, mode, M, N, K, ldx):
         assert int(ws[256:o].count_nonzero()) == 0, "split-K workspace not restored"
 
 
-def test_fused_linear_in_cuda_graph(gpu_lib):
-    """The fused kernel replayed from a CUDA graph (frozen arguments, same workspace every replay)
-    with changing activations: every replay quantizes the new X and matches the oracle."""
+@pytest.mark.parametrize("path", ["fused", "two"])
+def test_fused_linear_in_cuda_graph(gpu_lib, monkeypatch, path):
+    """w4a8_linear (fused kernel, or quantizer + GEMM) replayed from a CUDA graph (frozen arguments,
+    same workspace every replay) with changing activations: every replay quantizes the new X and
+    matches the oracle."""
+    if path == "fused":
+        monkeypatch.setenv("QOQ_LINEAR_FUSED", "1")
+    else:
+        monkeypatch.delenv("QOQ_LINEAR_FUSED", raising=False)
     M, N, K = 64, 1280, 1024
     X0, p_ref, s0_ref, *_ = _fused_case(M, N, K, K, seed=77)
     packed, s0 = to_dev(p_ref), to_dev(s0_ref)
