@@ -23,6 +23,7 @@ _lock = threading.Lock()
 _lib = None
 
 TILE_BYTES = 8448
+PC_TILE_BYTES = 8192
 
 
 def build(force: bool = False) -> str:
@@ -58,6 +59,10 @@ def lib() -> ctypes.CDLL:
                 "oracle_epilogue_f64": (I, [P, P, P, I, I, P]),
                 "oracle_linear_rows": (I, [P, I, I, I, I, P, P, I, P]),
                 "oracle_num_threads": (I, []),
+                "oracle_pc_quantize": (I, [P, I, I, P, P, P]),
+                "oracle_pc_pack": (I, [P, I, I, P]),
+                "oracle_pc_unpack": (I, [P, I, I, P]),
+                "oracle_pc_gemm_i32": (I, [P, P, P, I, I, I, P]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -226,3 +231,54 @@ def linear_rows(X: np.ndarray, packed: np.ndarray, s0: np.ndarray, N: int,
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+# ---- NEXT-1: per-channel W4A8 (§5.2.2) ----
+
+def pc_quantize(W: np.ndarray):
+    """PC1 (Eq. 2, per-channel P:134, FP16 scale P:447): -> (qu4 [N][K], s_w fp16 [N], z_w uint8 [N])."""
+    W = _u16(W)
+    N, K = W.shape
+    qu4 = np.empty((N, K), np.uint8)
+    s = np.empty(N, np.uint16)
+    z = np.empty(N, np.uint8)
+    _check(lib().oracle_pc_quantize(_p(W), N, K, _p(qu4), _p(s), _p(z)), "pc_quantize")
+    return qu4, s.view(np.float16), z
+
+
+def pc_pack(qu4: np.ndarray) -> np.ndarray:
+    """The O3 nibble stream without level-2 bytes: (N/128)*(K/128)*8192 bytes."""
+    qu4 = np.ascontiguousarray(qu4, np.uint8)
+    N, K = qu4.shape
+    out = np.empty(max(1, (N // 128) * (K // 128) * PC_TILE_BYTES), np.uint8)
+    _check(lib().oracle_pc_pack(_p(qu4), N, K, _p(out)), "pc_pack")
+    return out
+
+
+def pc_unpack(packed: np.ndarray, N: int, K: int) -> np.ndarray:
+    packed = np.ascontiguousarray(packed, np.uint8)
+    qu4 = np.empty((N, K), np.uint8)
+    _check(lib().oracle_pc_unpack(_p(packed), N, K, _p(qu4)), "pc_unpack")
+    return qu4
+
+
+def pc_quantize_weights(W: np.ndarray):
+    """PC1 -> pack: the per-channel offline packer. -> (packed uint8, s_w fp16 [N], z_w uint8 [N])."""
+    qu4, s, z = pc_quantize(W)
+    return pc_pack(qu4), s, z
+
+
+def pc_gemm_i32(qx: np.ndarray, qu4: np.ndarray, z_w: np.ndarray) -> np.ndarray:
+    """Eq. (per_channel_qmm) P:454 in integers: acc = sum_k qx (qu4 - z_w) (exact int32)."""
+    qx = np.ascontiguousarray(qx, np.int8)
+    qu4 = np.ascontiguousarray(qu4, np.uint8)
+    z_w = np.ascontiguousarray(z_w, np.uint8)
+    M, K = qx.shape
+    N = qu4.shape[0]
+    acc = np.empty((M, N), np.int32)
+    _check(lib().oracle_pc_gemm_i32(_p(qx), _p(qu4), _p(z_w), M, N, K, _p(acc)), "pc_gemm_i32")
+    return acc
+
+
+def pc_acc_from_packed(qx: np.ndarray, packed: np.ndarray, z_w: np.ndarray, N: int, K: int) -> np.ndarray:
+    return pc_gemm_i32(qx, pc_unpack(packed, N, K), z_w)

@@ -282,3 +282,95 @@ done:
     free(qu4); free(su8); free(z); free(qhat); free(qx); free(sx); free(acc);
     return rc;
 }
+
+/* ---------------- NEXT-1: per-channel W4A8 (§5.2.2) ---------------- */
+
+/* Round half away from zero of a double (Q1), as an int. */
+static int rha_d(double v) { return (int)round(v); }
+
+int oracle_pc_quantize(const uint16_t* W, int N, int K, uint8_t* qu4, uint16_t* s_w, uint8_t* z_w) {
+    if (N < 0 || K <= 0) return -1;
+    for (int n = 0; n < N; ++n) {
+        const uint16_t* w = W + (size_t)n * K;
+        float lo = oracle_h2f(w[0]), hi = lo;
+        for (int k = 1; k < K; ++k) {
+            float v = oracle_h2f(w[k]);
+            if (v < lo) lo = v;
+            if (v > hi) hi = v;
+        }
+        /* Eq. 2: s = (X_max - X_min) / (q_max - q_min), stored as fp16 (Q20) */
+        float range = hi - lo;
+        uint16_t sh;
+        if (range == 0.0f) {
+            sh = 0x3c00;                                  /* 1.0 */
+        } else {
+            sh = oracle_f2h_rn(range / 15.0f);
+            if ((sh & 0x7fff) == 0) sh = 0x0001;          /* 2^-24 */
+        }
+        float s = oracle_h2f(sh);
+        /* z = ⌈q_min - X_min / s⌋, q_min = 0, clamped to the u4 range (Q21) */
+        int z = clampi(rha_d(-(double)(lo / s)), 0, 15);
+        /* Q = ⌈X / s + z⌋ clamped to [0, 15] (Q22: t = fp32(X / s), t + z exact) */
+        for (int k = 0; k < K; ++k) {
+            float t = oracle_h2f(w[k]) / s;
+            qu4[(size_t)n * K + k] = (uint8_t)clampi(rha_d((double)t + (double)z), 0, 15);
+        }
+        s_w[n] = sh;
+        z_w[n] = (uint8_t)z;
+    }
+    return 0;
+}
+
+#define PC_TILE_BYTES 8192
+
+int oracle_pc_pack(const uint8_t* qu4, int N, int K, uint8_t* packed) {
+    if (!pack_shape_ok(N, K, 128)) return -1;
+    int KT = K / TILE_K;
+    for (int nt = 0; nt < N / TILE_N; ++nt)
+        for (int j = 0; j < KT; ++j) {
+            uint8_t* tile = packed + ((size_t)nt * KT + j) * PC_TILE_BYTES;
+            for (int r = 0; r < TILE_N; ++r) {
+                const uint8_t* q = qu4 + (size_t)(nt * TILE_N + r) * K + (size_t)j * TILE_K;
+                for (int c = 0; c < 4; ++c)
+                    for (int b = 0; b < 16; ++b)
+                        tile[c * 2048 + r * 16 + b] =
+                            (uint8_t)((q[32 * c + b] & 15) | ((q[32 * c + 16 + b] & 15) << 4));
+            }
+        }
+    return 0;
+}
+
+int oracle_pc_unpack(const uint8_t* packed, int N, int K, uint8_t* qu4) {
+    if (!pack_shape_ok(N, K, 128)) return -1;
+    int KT = K / TILE_K;
+    for (int nt = 0; nt < N / TILE_N; ++nt)
+        for (int j = 0; j < KT; ++j) {
+            const uint8_t* tile = packed + ((size_t)nt * KT + j) * PC_TILE_BYTES;
+            for (int r = 0; r < TILE_N; ++r) {
+                uint8_t* q = qu4 + (size_t)(nt * TILE_N + r) * K + (size_t)j * TILE_K;
+                for (int c = 0; c < 4; ++c)
+                    for (int b = 0; b < 16; ++b) {
+                        uint8_t byte = tile[c * 2048 + r * 16 + b];
+                        q[32 * c + b] = byte & 15;
+                        q[32 * c + 16 + b] = byte >> 4;
+                    }
+            }
+        }
+    return 0;
+}
+
+int oracle_pc_gemm_i32(const int8_t* qx, const uint8_t* qu4, const uint8_t* z_w, int M, int N, int K,
+                       int32_t* acc) {
+    if (M < 0 || N < 0 || K <= 0) return -1;
+    int overflow = 0;
+#pragma omp parallel for collapse(2) schedule(static) reduction(|:overflow)
+    for (int m = 0; m < M; ++m)
+        for (int n = 0; n < N; ++n) {
+            int64_t s = 0;
+            for (int k = 0; k < K; ++k)
+                s += (int64_t)qx[(size_t)m * K + k] * ((int64_t)qu4[(size_t)n * K + k] - (int64_t)z_w[n]);
+            if (s > INT32_MAX || s < INT32_MIN) overflow = 1;
+            acc[(size_t)m * N + n] = (int32_t)s;
+        }
+    return overflow ? -2 : 0;
+}

@@ -80,6 +80,30 @@ int oracle_epilogue_f64(const int32_t* acc, const uint16_t* sx, const uint16_t* 
 int oracle_linear_rows(const uint16_t* X, int K, int ldx, int m0, int m1,
                        const uint8_t* packed, const uint16_t* s0, int N, double* y);
 
+/* ---------------- NEXT-1: per-channel W4A8 (§5.2.2) ---------------- */
+
+/* PC1 — per-output-channel asymmetric UINT4 weight quantization: Eq. 2 with
+ * q_min = 0, q_max = 15, s and z shared within each row (per-channel), FP16 scale
+ * ("first-level FP16 scaling"). Readings (Q20-Q22):
+ *   range = fp32(max_k W) - fp32(min_k W) (IEEE fp32 subtraction);
+ *   s = fp16_rn(range / 15.0f) (fp32 division); range == 0 -> 1.0; fp16 underflow -> 2^-24;
+ *   z = clamp(⌈0 - t_min⌋, 0, 15), t_min = fp32(min / s) with the fp16-rounded s (Q1: ⌈·⌋ rounds
+ *       half away from zero);
+ *   q = clamp(⌈t + z⌋, 0, 15), t = fp32(W / s), t + z summed exactly (in double).
+ * W: [N][K] fp16. qu4: [N][K] in [0,15]; s_w: [N] fp16; z_w: [N] in [0,15]. */
+int oracle_pc_quantize(const uint16_t* W, int N, int K, uint8_t* qu4, uint16_t* s_w, uint8_t* z_w);
+
+/* PC pack: the O3 nibble stream without level-2 bytes — 128x128 tiles of 8192 bytes, n-tile-major,
+ * chunk c / row r at c*2048 + r*16, byte b = q[32c+b] | q[32c+16+b] << 4 (Q15). */
+int oracle_pc_pack(const uint8_t* qu4, int N, int K, uint8_t* packed);
+int oracle_pc_unpack(const uint8_t* packed, int N, int K, uint8_t* qu4);
+
+/* PC GEMM, the definition Eq. (per_channel_qmm) P:454 in integers: acc[m][n] =
+ * sum_k qx[m][k] * (qu4[n][k] - z_w[n]), accumulated in int64 and checked into int32 (-2 if not).
+ * The epilogue reference is oracle_epilogue_f64(acc, s_x, s_w): y = acc * s_x[m] * s_w[n]. */
+int oracle_pc_gemm_i32(const int8_t* qx, const uint8_t* qu4, const uint8_t* z_w, int M, int N, int K,
+                       int32_t* acc);
+
 /* Number of OpenMP threads the oracle's parallel loops use (1 without OpenMP). */
 int oracle_num_threads(void);
 

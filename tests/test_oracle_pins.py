@@ -352,3 +352,100 @@ def test_linear_rows_subset_equals_full():
     full = oracle.linear_rows(X, packed, s0, 128)
     part = oracle.linear_rows(X, packed, s0, 128, 3, 7)
     assert np.array_equal(full[3:7], part)
+
+
+# ------------------------------------------------------------------ NEXT-1: per-channel W4A8 (§5.2.2)
+
+def test_pc_quantize_exact_grid_reproduces():
+    """Eq. 2 on rows that ARE an asymmetric u4 grid: W = (q - z) * s with s a power of
+    two and every code 0..15 present, so min/max give range = 15 s exactly. PC1 must recover s, z
+    and every q (the closed form; any sign / offset / rounding slip breaks it)."""
+    rng = np.random.default_rng(11)
+    N, K = 6, 64
+    s_true = [2.0 ** -6, 2.0 ** -3, 0.5, 2.0 ** -10, 1.0, 2.0 ** -4]
+    z_true = [7, 0, 15, 3, 9, 12]
+    q_true = rng.integers(0, 16, size=(N, K))
+    q_true[:, 0], q_true[:, 1] = 0, 15                      # min and max codes present
+    W = ((q_true - np.array(z_true)[:, None]) * np.array(s_true)[:, None]).astype(np.float16)
+    qu4, s, z = oracle.pc_quantize(W)
+    assert np.array_equal(s.astype(np.float64), np.array(s_true))
+    assert list(z) == z_true
+    assert np.array_equal(qu4, q_true)
+
+
+def test_pc_quantize_bounds_and_invariants():
+    """Every code in [0, 15], z in [0, 15]; when the rounded code is not clamped the dequantized
+    weight (q - z) s is within s/2 of W (round-to-nearest of Eq. 2); the row's min and max map to
+    the end codes up to one step (the zero point absorbs the offset)."""
+    W = synth.weights_fp16(64, 512, seed=3)
+    qu4, s, z = oracle.pc_quantize(W)
+    assert qu4.min() >= 0 and qu4.max() <= 15 and z.max() <= 15
+    sd = s.astype(np.float64)[:, None]
+    Wd = W.astype(np.float64)
+    t = Wd / sd + z[:, None]
+    inside = (t > -0.5) & (t < 15.5)
+    err = np.abs(Wd - (qu4.astype(np.float64) - z[:, None]) * sd)
+    assert np.all(err[inside] <= sd.repeat(W.shape[1], 1)[inside] / 2 * (1 + 2e-6))
+    assert np.all(qu4.min(1) <= 1) and np.all(qu4.max(1) >= 14)
+
+
+def test_pc_quantize_half_away_ties_and_degenerate_rows():
+    """Q1 in Eq. 2: a weight exactly half a step off the grid rounds AWAY from zero in t + z
+    (t + z = 2.5 -> 3, not 2 as half-even or half-down would give); a constant row has range 0 ->
+    s = 1 (Q20) and codes from z = ⌈-min⌋ clamped; an all-zero row quantizes to z = 0, q = 0."""
+    s_ = 2.0 ** -4
+    row = np.array([0, 15, 4.5, 0.5, 1.5, 7.5], np.float64)       # codes offset by z = 0 -> t + z
+    W = np.zeros((3, 128), np.float16)
+    W[0, :6] = (row * s_).astype(np.float16)
+    W[0, 6:] = 0
+    W[1, :] = np.float16(0.25)
+    qu4, s, z = oracle.pc_quantize(W)
+    assert float(s[0]) == s_ and z[0] == 0
+    assert list(qu4[0, :6]) == [0, 15, 5, 1, 2, 8]                # 4.5 -> 5, 0.5 -> 1, 7.5 -> 8
+    assert float(s[1]) == 1.0 and z[1] == 0 and np.all(qu4[1] == 0)   # ⌈0.25⌋ = 0
+    assert float(s[2]) == 1.0 and z[2] == 0 and np.all(qu4[2] == 0)
+
+
+def test_pc_pack_is_the_o3_nibble_stream_and_roundtrips():
+    """The per-channel tile is byte-for-byte the first 8192 bytes of the pinned O3 tile for the
+    same codes (P:447 interleave, Q15), and pc_unpack inverts pc_pack."""
+    rng = np.random.default_rng(5)
+    N, K = 256, 384
+    q = rng.integers(0, 16, size=(N, K)).astype(np.uint8)
+    pc = oracle.pc_pack(q)
+    o3 = oracle.pack(q, np.ones((N, K // 128), np.uint8), np.zeros((N, K // 128), np.uint8))
+    tiles_pc = pc.reshape(-1, 8192)
+    tiles_o3 = o3.reshape(-1, 8448)[:, :8192]
+    assert np.array_equal(tiles_pc, tiles_o3)
+    assert np.array_equal(oracle.pc_unpack(pc, N, K), q)
+
+
+def test_pc_gemm_equals_subtraction_after_multiplication():
+    """Eq. (per_channel_qmm_step2/3) P:466-478 in integers: sum_k qx (q - z) == (Q_X Q_W) - z t_X
+    with t_X = sum_k qx (the exact form of the paper's t_X, Q19). The right side is computed with
+    the pinned O5 GEMM on q as-is and the pinned O4 row sums — a different route from PC's
+    definition — and must agree exactly; int32 overflow is detected."""
+    X = synth.activations_fp16(16, 256, seed=9)
+    W = synth.weights_fp16(128, 256, seed=9)
+    qx, sx, tx = oracle.quantize_activations(X)
+    qu4, s, z = oracle.pc_quantize(W)
+    acc = oracle.pc_gemm_i32(qx, qu4, z)
+    rhs = oracle.gemm_i32(qx, qu4.astype(np.int16)).astype(np.int64) - np.outer(tx, z.astype(np.int64))
+    assert np.array_equal(acc.astype(np.int64), rhs)
+    big = np.full((1, 1200000), 127, np.int8)           # 127 * 15 * 1.2e6 > 2^31
+    with pytest.raises(ValueError):
+        oracle.pc_gemm_i32(big, np.full((1, 1200000), 15, np.uint8), np.zeros(1, np.uint8))
+
+
+def test_pc_linear_approximates_float_gemm():
+    """Sanity envelope (not parity): per-channel W4A8 of a float GEMM, y = acc s_x s_w, is within a
+    few tens of percent (relative Frobenius) of the unquantized product — 4-bit per-channel weights
+    are coarser than the g128 path but still track it."""
+    X = synth.activations_fp16(16, 512, seed=1)
+    W = synth.weights_fp16(256, 512, seed=1)
+    qx, sx, tx = oracle.quantize_activations(X)
+    qu4, s, z = oracle.pc_quantize(W)
+    y = oracle.epilogue_f64(oracle.pc_gemm_i32(qx, qu4, z), sx, s)
+    ref = X.astype(np.float64) @ W.astype(np.float64).T
+    rel = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+    assert 0.02 < rel < 0.35, rel
