@@ -40,7 +40,7 @@ typedef enum {
 const char* qoq_status_string(int status);
 /* ABI version of this header (incremented on any signature or layout change). */
 int qoq_abi_version(void);
-#define QOQ_ABI_VERSION 2
+#define QOQ_ABI_VERSION 3
 
 /* ----------------------------------------------------------------------------------------------
  * Packed weight layout (frozen). The B200 form of "store the weights in the order
@@ -139,8 +139,30 @@ int qoq_linear_host(const void* X_host_fp16, int M, int K,
                     const void* packed, const void* s0_fp16, int N,
                     void* Y_host_fp16, void* dev_scratch, size_t scratch_bytes, void* stream);
 
+/* ---- Per-channel W4A8 (the paper's other precision mode, §5.2.2; NEXT-1) ----
+ * Weights: per-output-channel asymmetric UINT4 (Eq. 2, q_min = 0, q_max = 15) with an
+ * FP16 scale s_w[n] and a u8 zero point z_w[n] in [0,15]; no level-2 parameters. The GEMM unpacks
+ * the codes in the main loop (lanes = q_u4, unsigned 8-bit MMA operand) and applies the zero point
+ * AFTER the multiplication, in the epilogue (exact t_x = Σ_k q_x, Q19):
+ *   Y[m][n] = fp16( s_x[m] · s_w[n] · (Σ_k q_x[m][k] q_u4[n][k] − z_w[n] · t_x[m]) ).
+ * Packed layout: the tile stream above without the 256 level-2 bytes (8192-byte tiles).
+ * Shapes and errors as qoq_quantize_weights / qoq_w4a8_gemm; t_x is REQUIRED (the quantizer's row
+ * sums) and z_w must be 4-byte aligned, else QOQ_ERR_INVALID_ARG. Workspace: qoq_gemm_workspace_bytes.
+ * W [N][K] fp16; s_w_fp16 [N] and z_w [N] are outputs of the packer, inputs of the GEMM. */
+size_t qoq_pc_packed_weight_bytes(int N, int K);
+int qoq_pc_quantize_weights(const void* W_fp16, int N, int K, void* packed, size_t packed_bytes,
+                            void* s_w_fp16, uint8_t* z_w, void* stream);
+int qoq_pc_w4a8_gemm(const int8_t* qx, const void* sx_fp16, const int32_t* tx, const void* packed,
+                     const void* s_w_fp16, const uint8_t* z_w, int M, int N, int K,
+                     void* Y_fp16, int ldy, void* workspace, size_t workspace_bytes, void* stream);
+/* parity entry: the exact INT32 Σ_k q_x (q_u4 − z_w) into acc [M][ldacc] (ldacc % 4 == 0) */
+int qoq_pc_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed, const uint8_t* z_w,
+                         int M, int N, int K, int32_t* acc, int ldacc,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 /* Kernels launched per successful call (launch accounting for benchmarks):
  * quantize_weights 2, quantize_activations_per_token 1, w4a8_gemm 1, w4a8_gemm_i32 1,
+ * pc_quantize_weights 2, pc_w4a8_gemm 1, pc_w4a8_gemm_i32 1,
  * w4a8_linear 2 (1 when fused: QOQ_LINEAR_FUSED=1 and M <= 64), linear_host as w4a8_linear
  * (plus 2 async copies). */
 

@@ -23,10 +23,10 @@ LIB_PATH = os.path.join(_HERE, "libqoq_b200.so" if not os.environ.get("QOQ_LIB_V
                         else f"libqoq_b200_{os.environ['QOQ_LIB_VARIANT']}.so")
 GROUP = 128
 TILE_BYTES = 8448
-ABI_VERSION = 2
+ABI_VERSION = 3
 # kernels launched per call (matches include/qoq_b200.h)
 LAUNCHES = {"quantize_weights": 2, "quantize_activations_per_token": 1, "w4a8_gemm": 1,
-            "w4a8_gemm_i32": 1}
+            "w4a8_gemm_i32": 1, "pc_quantize_weights": 2, "pc_w4a8_gemm": 1, "pc_w4a8_gemm_i32": 1}
 FUSE_MAX_M = 64   # w4a8_linear / linear_host with QOQ_LINEAR_FUSED=1: one fused kernel up to this M
 
 
@@ -72,6 +72,10 @@ def load() -> ctypes.CDLL:
             "qoq_w4a8_linear": (I, [P, I, I, I, I, I, P, P, P, I, P, Z, P]),
             "qoq_linear_host_scratch_bytes": (Z, [I, I, I]),
             "qoq_linear_host": (I, [P, I, I, P, P, I, P, P, Z, P]),
+            "qoq_pc_packed_weight_bytes": (Z, [I, I]),
+            "qoq_pc_quantize_weights": (I, [P, I, I, P, Z, P, P, P]),
+            "qoq_pc_w4a8_gemm": (I, [P, P, P, P, P, P, I, I, I, P, I, P, Z, P]),
+            "qoq_pc_w4a8_gemm_i32": (I, [P, P, P, P, I, I, I, P, I, P, Z, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -255,3 +259,49 @@ def linear_host(X_host: torch.Tensor, packed: torch.Tensor, s0: torch.Tensor, N:
            load().qoq_linear_host(ctypes.c_void_p(X_host.data_ptr()), M, K, _ptr(packed), _ptr(s0), N,
                                   ctypes.c_void_p(Y_host.data_ptr()), _ptr(scratch), scratch.numel(),
                                   _stream(stream)))
+
+
+# ------------------------------------------------------------------ per-channel W4A8 (NEXT-1, §5.2.2)
+
+def pc_packed_weight_bytes(N: int, K: int) -> int:
+    return load().qoq_pc_packed_weight_bytes(N, K)
+
+
+def pc_quantize_weights(W: torch.Tensor, stream=None):
+    """W [N][K] fp16 (cuda) -> (packed uint8 8192-byte tiles, s_w fp16 [N], z_w uint8 [N])."""
+    if W.dtype != torch.float16 or W.dim() != 2:
+        raise ValueError("W must be a 2-D fp16 tensor")
+    N, K = W.shape
+    nbytes = pc_packed_weight_bytes(N, K)
+    packed = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=W.device)
+    s_w = torch.empty(N, dtype=torch.float16, device=W.device)
+    z_w = torch.empty(max(N, 4), dtype=torch.uint8, device=W.device)
+    _check("qoq_pc_quantize_weights",
+           load().qoq_pc_quantize_weights(_ptr(W), N, K, _ptr(packed), nbytes, _ptr(s_w), _ptr(z_w),
+                                          _stream(stream)))
+    return packed[:nbytes], s_w, z_w[:N]
+
+
+def pc_w4a8_gemm(qx: torch.Tensor, sx: torch.Tensor, tx: torch.Tensor, packed: torch.Tensor, s_w: torch.Tensor,
+                 z_w: torch.Tensor, N: int, out: torch.Tensor | None = None, workspace: Workspace | None = None,
+                 stream=None) -> torch.Tensor:
+    """Y [M][N] fp16 = fp16(s_x[m] s_w[n] (Σ_k qx q_u4 − z_w[n] t_x[m]))."""
+    M, K = qx.shape
+    Y = torch.empty(M, N, dtype=torch.float16, device=qx.device) if out is None else out
+    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace)
+    _check("qoq_pc_w4a8_gemm",
+           load().qoq_pc_w4a8_gemm(_ptr(qx), _ptr(sx), _ptr(tx), _ptr(packed), _ptr(s_w), _ptr(z_w), M, N, K,
+                                   _ptr(Y), Y.stride(0), _ptr(ws), wsb, _stream(stream)))
+    return Y
+
+
+def pc_w4a8_gemm_i32(qx: torch.Tensor, tx: torch.Tensor, packed: torch.Tensor, z_w: torch.Tensor, N: int,
+                     workspace: Workspace | None = None, stream=None) -> torch.Tensor:
+    """Exact INT32 Σ_k qx (q_u4 − z_w) [M][N] (parity entry)."""
+    M, K = qx.shape
+    acc = torch.empty(M, N, dtype=torch.int32, device=qx.device)
+    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace)
+    _check("qoq_pc_w4a8_gemm_i32",
+           load().qoq_pc_w4a8_gemm_i32(_ptr(qx), _ptr(tx), _ptr(packed), _ptr(z_w), M, N, K, _ptr(acc), N,
+                                       _ptr(ws), wsb, _stream(stream)))
+    return acc

@@ -42,11 +42,14 @@ int num_sms_or_default() {
 
 int run_gemm(const int8_t* qx, const void* sx, const int32_t* tx, const void* packed, const void* s0,
              int M, int N, int K, int group, void* out, int ldo, bool out_i32,
-             void* ws, size_t ws_bytes, cudaStream_t st, void* trace = nullptr) {
+             void* ws, size_t ws_bytes, cudaStream_t st, void* trace = nullptr, const uint8_t* zw = nullptr,
+             bool pc = false) {
     int rc = gemm_shape_status(M, N, K, group);
     if (rc) return rc;
     if (M == 0) return QOQ_OK;
     if (!qx || !packed || !out || (!out_i32 && (!sx || !s0))) return QOQ_ERR_INVALID_ARG;
+    // per-channel W4A8: t_x (the zero-point term) and the 4-byte-aligned zero points are required
+    if (pc && (!tx || !zw || (reinterpret_cast<uintptr_t>(zw) & 3u))) return QOQ_ERR_INVALID_ARG;
     if (!aligned16(qx) || !aligned16(packed) || ldo < N) return QOQ_ERR_INVALID_ARG;
     // vectorized epilogue: 4 consecutive outputs per store, 8-byte aligned s0 loads
     if (ldo % 4 != 0 || !aligned16(out) || (!out_i32 && !aligned16(s0))) return QOQ_ERR_INVALID_ARG;
@@ -54,7 +57,9 @@ int run_gemm(const int8_t* qx, const void* sx, const int32_t* tx, const void* pa
     if ((rc = check_arch(&sms))) return rc;
     GemmPlan p = plan_gemm(M, N, K, sms);
     if (p.ws_bytes > 0 && (!ws || ws_bytes < p.ws_bytes || !aligned16(ws))) return QOQ_ERR_WORKSPACE;
+    if (pc && p.CG != 1) return QOQ_ERR_UNSUPPORTED;   // the CTA-pair variant is g128 only
     GemmArgs a{qx, sx, tx, packed, s0, out, ldo, out_i32, M, N, K, p.ws_bytes ? ws : nullptr, trace};
+    a.zw = pc ? zw : nullptr;
     return launch_w4a8_gemm(a, p, st, /*pdl=*/true) == cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
 }
 
@@ -193,6 +198,40 @@ size_t qoq_linear_workspace_bytes(int M, int N, int K) {
 int qoq_w4a8_linear(const void* X, int ldx, int M, int N, int K, int group, const void* packed, const void* s0,
                     void* Y, int ldy, void* ws, size_t ws_bytes, void* stream) {
     return run_linear(X, ldx, M, N, K, group, packed, s0, Y, ldy, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+// ---- per-channel W4A8 (NEXT-1, §5.2.2)
+
+size_t qoq_pc_packed_weight_bytes(int N, int K) {
+    if (N <= 0 || K <= 0 || N % kTileN || K % kTileK) return 0;
+    return (size_t)(N / kTileN) * (size_t)(K / kTileK) * kPcTileBytes;
+}
+
+int qoq_pc_quantize_weights(const void* W, int N, int K, void* packed, size_t packed_bytes, void* s_w,
+                            uint8_t* z_w, void* stream) {
+    if (N <= 0 || K <= 0) return QOQ_ERR_INVALID_ARG;
+    if (N % kTileN || K % kTileK) return QOQ_ERR_SHAPE;
+    if (!W || !packed || !s_w || !z_w || !aligned16(W) || !aligned16(packed)) return QOQ_ERR_INVALID_ARG;
+    if (packed_bytes < qoq_pc_packed_weight_bytes(N, K)) return QOQ_ERR_WORKSPACE;
+    int rc = check_arch(nullptr);
+    if (rc) return rc;
+    return launch_pc_quantize_weights(W, N, K, packed, s_w, z_w, static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
+int qoq_pc_w4a8_gemm(const int8_t* qx, const void* sx, const int32_t* tx, const void* packed, const void* s_w,
+                     const uint8_t* z_w, int M, int N, int K, void* Y, int ldy, void* ws, size_t ws_bytes,
+                     void* stream) {
+    if (ldy < N) return QOQ_ERR_INVALID_ARG;
+    return run_gemm(qx, sx, tx, packed, s_w, M, N, K, 128, Y, ldy, false, ws, ws_bytes,
+                    static_cast<cudaStream_t>(stream), nullptr, z_w, true);
+}
+
+int qoq_pc_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed, const uint8_t* z_w, int M,
+                         int N, int K, int32_t* acc, int ldacc, void* ws, size_t ws_bytes, void* stream) {
+    if (ldacc < N) return QOQ_ERR_INVALID_ARG;
+    return run_gemm(qx, nullptr, tx, packed, nullptr, M, N, K, 128, acc, ldacc, true, ws, ws_bytes,
+                    static_cast<cudaStream_t>(stream), nullptr, z_w, true);
 }
 
 // Debug (not in the public header): the fp16 GEMM with a per-CTA %globaltimer trace

@@ -11,6 +11,7 @@ namespace qoq {
 constexpr int kTileN = 128;          // output channels per packed tile (MMA M)
 constexpr int kTileK = 128;          // input channels per packed tile (= group size g)
 constexpr int kTileBytes = 8448;     // 8192 B of u4 codes + 128 B s_u8 + 128 B z*s_u8
+constexpr int kPcTileBytes = 8192;   // per-channel W4A8 (NEXT-1): the u4 codes only
 
 // Work decomposition of one GEMM launch (host planner <-> kernel scheduler).
 struct GemmPlan {
@@ -46,12 +47,17 @@ struct GemmArgs {
     const void* X = nullptr;
     int ldx = 0;
     int* qsync = nullptr;
+    // per-channel W4A8 (NEXT-1): packed holds 8192-byte code tiles, s0 is s_w, zw the u8 zero points;
+    // Y = s_x s_w (acc - z_w t_x) (tx required)
+    const uint8_t* zw = nullptr;
 };
 
 constexpr int kFuseMaxM = 64;   // above: quantizer kernel + GEMM (the prologue would serialize M rows)
 
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl);
 cudaError_t launch_quantize_weights(const void* W, int N, int K, void* packed, void* s0, cudaStream_t st);
+cudaError_t launch_pc_quantize_weights(const void* W, int N, int K, void* packed, void* s_w, uint8_t* z_w,
+                                       cudaStream_t st);
 cudaError_t launch_quantize_activations(const void* X, int M, int K, int ldx, int8_t* qx, void* sx,
                                         int32_t* tx, cudaStream_t st, bool pdl);
 

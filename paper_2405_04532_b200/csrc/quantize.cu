@@ -33,6 +33,21 @@ __device__ __forceinline__ float block_reduce_max(float v, float* red) {
     return v;  // valid in every thread
 }
 
+// block max of arbitrary-sign values (identity -inf; block_reduce_max above assumes v >= 0)
+__device__ __forceinline__ float block_reduce_max_signed(float v, float* red) {
+    const float ninf = -__int_as_float(0x7f800000);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    v = (l < nw) ? red[l] : ninf;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;  // valid in every thread
+}
+
 __device__ __forceinline__ int block_reduce_sum(int v, int* red) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -124,6 +139,78 @@ __global__ void __launch_bounds__(128) level2_pack_kernel(const __half* __restri
     tile[8320 + r] = (uint8_t)(z * su);
 }
 
+// ------------------------------------------------------------------ weights, per-channel W4A8 (NEXT-1)
+// Per-output-channel asymmetric UINT4 (Eq. 2, q_min = 0, q_max = 15; FP16 scale P:447;
+// readings Q20-Q22 in DESIGN.md §3): s_w = fp16(fp32(max - min) / 15), z = clamp(⌈-min / s_w⌋, 0, 15),
+// q = clamp(⌈fp32(W / s_w) + z⌋, 0, 15) with t + z summed exactly (double; offline, cost irrelevant).
+
+__global__ void __launch_bounds__(256) pc_scale_kernel(const __half* __restrict__ W, int K,
+                                                       __half* __restrict__ s_w, uint8_t* __restrict__ z_w) {
+    __shared__ float red[32];
+    pdl_wait();
+    const __half* row = W + (size_t)blockIdx.x * K;
+    float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);   // +-inf
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+        const float v = __half2float(row[i]);
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+    }
+    hi = block_reduce_max_signed(hi, red);
+    lo = -block_reduce_max_signed(-lo, red);
+    if (threadIdx.x == 0) {
+        const float range = hi - lo;
+        __half sh;
+        if (range == 0.0f) {
+            sh = __float2half_rn(1.0f);
+        } else {
+            sh = __float2half_rn(__fdiv_rn(range, 15.0f));
+            if (__half_as_ushort(sh) == 0) sh = __ushort_as_half((unsigned short)1);   // 2^-24
+        }
+        const float s = __half2float(sh);
+        const int z = min(15, max(0, (int)round(-(double)__fdiv_rn(lo, s))));
+        s_w[blockIdx.x] = sh;
+        z_w[blockIdx.x] = (uint8_t)z;
+    }
+}
+
+// grid (K/128, N/128), 128 threads: thread r owns output channel n = 128*blockIdx.y + r and writes
+// the 4 x 16 B of codes of k-tile blockIdx.x (the g128 tile's nibble layout, 8192-byte tiles).
+__global__ void __launch_bounds__(128) pc_pack_kernel(const __half* __restrict__ W, int K,
+                                                      const __half* __restrict__ s_w,
+                                                      const uint8_t* __restrict__ z_w,
+                                                      uint8_t* __restrict__ packed) {
+    pdl_wait();
+    const int j = blockIdx.x, nt = blockIdx.y, r = threadIdx.x;
+    const int n = nt * 128 + r, KT = K / 128;
+    const float s = __half2float(s_w[n]);
+    const double z = (double)z_w[n];
+    const uint4* src = reinterpret_cast<const uint4*>(W + (size_t)n * K + (size_t)j * 128);
+    uint8_t* tile = packed + ((size_t)nt * KT + j) * 8192;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+        int code[32];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            uint4 u = __ldg(src + c * 4 + v);
+            const __half* h = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                code[v * 8 + e] = min(15, max(0, (int)round((double)__fdiv_rn(__half2float(h[e]), s) + z)));
+        }
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            w[i] = 0;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                const int b = 4 * i + bb;
+                w[i] |= (uint32_t)(code[b] | (code[b + 16] << 4)) << (8 * bb);
+            }
+        }
+        *reinterpret_cast<uint4*>(tile + c * 2048 + r * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
 // ------------------------------------------------------------------ activations
 
 // One CTA per token row: the row (K <= 8 * kQThreads * kQVec) is read ONCE into registers with all
@@ -188,6 +275,17 @@ cudaError_t launch_quantize_weights(const void* W, int N, int K, void* packed, v
     level2_pack_kernel<<<dim3(K / 128, N / 128), 128, 0, st>>>(static_cast<const __half*>(W), K,
                                                                 static_cast<const __half*>(s0),
                                                                 static_cast<uint8_t*>(packed));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pc_quantize_weights(const void* W, int N, int K, void* packed, void* s_w, uint8_t* z_w,
+                                       cudaStream_t st) {
+    pc_scale_kernel<<<N, 256, 0, st>>>(static_cast<const __half*>(W), K, static_cast<__half*>(s_w), z_w);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    pc_pack_kernel<<<dim3(K / 128, N / 128), 128, 0, st>>>(static_cast<const __half*>(W), K,
+                                                            static_cast<const __half*>(s_w), z_w,
+                                                            static_cast<uint8_t*>(packed));
     return cudaGetLastError();
 }
 

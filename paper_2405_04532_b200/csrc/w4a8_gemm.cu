@@ -68,8 +68,12 @@ struct Roles {
 // own TMEM and holds half of the activation rows; the leader issues cta_group::2 MMAs (M = 256) —
 // half the MMA instructions, handoffs and activation SMEM traffic per SM (tools/cta2_check.cu:
 // 32 cycles per 256x64x32 MMA vs 45.5 per 128x64x32 on one SM).
-template <int BN, int CG = 1>
+// PC = true: per-channel W4A8 (NEXT-1, §5.2.2): 8192-byte code tiles, no level-2 parameters; the
+// dequant only unpacks (lanes = q_u4, fed as UNSIGNED 8-bit A) and the epilogue applies the zero
+// point after the multiplication: Y = s_x s_w (acc - z_w t_x).
+template <int BN, int CG = 1, bool PC = false>
 struct Cfg {
+    static constexpr int kTB = PC ? kPcTileBytes : kTileBytes;        // bytes of one packed 128x128 tile
     // dequant groups: QOQ_DEQ_GROUPS (default 3; measured +1..9% over 2 at decode) where the TMEM budget allows a rotation-compatible
     // A ring, else 2
     static constexpr int kDeqGroups = (BN <= 64) ? QOQ_DEQ_GROUPS : 2;
@@ -123,7 +127,7 @@ struct Cfg {
 #else
     static constexpr int kXStages = (BN <= 64 && CG == 1) ? QOQ_XSTAGES : kXStagesDef;
 #endif
-    static constexpr int kWStageBytes = ((2 * kTileBytes + 1023) / 1024) * 1024;   // packed weights of one step
+    static constexpr int kWStageBytes = ((2 * kTB + 1023) / 1024) * 1024;   // packed weights of one step
     static constexpr int kWRaw = (212 * 1024 - kEpiBytes - kXStages * kXStageBytes) / kWStageBytes;
     static constexpr int kWCap = kWRaw > 12 ? 12 : kWRaw;
     static constexpr int kWStages = (kWCap / kDeqRot) * kDeqRot;
@@ -164,6 +168,7 @@ struct KParams {
     int8_t* qx_rows;             // q_x [M][K] (the tensor map's global buffer)
     int ldx, K;
     int* qsync;                  // [2] arrivals / departures; the last departure re-zeroes both
+    const uint8_t* zw;           // per-channel W4A8: z_w [N] (else nullptr)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -280,8 +285,8 @@ struct WProducer {
         if (QOQ_ABLATE & 4) {
             mbar_arrive(&wfull[ws]);
         } else {
-            mbar_arrive_expect_tx(&wfull[ws], nk * kTileBytes);
-            bulk_g2s(dst, p.packed + ((size_t)nt * p.KT + kt0) * kTileBytes, nk * kTileBytes, &wfull[ws], pol);
+            mbar_arrive_expect_tx(&wfull[ws], nk * C::kTB);
+            bulk_g2s(dst, p.packed + ((size_t)nt * p.KT + kt0) * C::kTB, nk * C::kTB, &wfull[ws], pol);
         }
         if (++ws == C::kWStages) { ws = 0; wph ^= 1; }
         if (++sg == s1) {
@@ -298,11 +303,24 @@ struct WProducer {
     }
 };
 
-// Four consecutive outputs Y[m][n..n+3] (or acc) from four INT32 accumulators.
+// The zero-point multipliers of four consecutive output rows: z_w[n..n+3] (per-channel), else 1
+// (the g128 path's bias 128·t_x applies to every row alike).
+template <bool PC>
+__device__ __forceinline__ void load_z4(const KParams& p, int n, int (&zv)[4]) {
+    if constexpr (PC) {
+        const uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(p.zw + n));
+        zv[0] = u & 255; zv[1] = (u >> 8) & 255; zv[2] = (u >> 16) & 255; zv[3] = u >> 24;
+    } else {
+        zv[0] = zv[1] = zv[2] = zv[3] = 1;
+    }
+}
+
+// Four consecutive outputs Y[m][n..n+3] (or acc) from four INT32 accumulators: acc - bias·zv, then
+// the s_x s0 outer-product scaling (per-channel: bias = t_x, zv = z_w).
 template <bool OUT_I32>
 __device__ __forceinline__ void write_out4(const KParams& p, int m, int n, int4 a, int bias, float sxf,
-                                           const float (&s0v)[4]) {
-    a.x -= bias; a.y -= bias; a.z -= bias; a.w -= bias;
+                                           const float (&s0v)[4], const int (&zv)[4]) {
+    a.x -= bias * zv[0]; a.y -= bias * zv[1]; a.z -= bias * zv[2]; a.w -= bias * zv[3];
     if constexpr (OUT_I32) {
         *reinterpret_cast<int4*>(static_cast<int32_t*>(p.out) + (size_t)m * p.ldo + n) = a;
     } else {
@@ -435,10 +453,10 @@ __device__ __forceinline__ void zero_acc(uint32_t taddr) {
     tmem_wait_st();
 }
 
-template <int BN, bool OUT_I32, int CG>
-__global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
+template <int BN, bool OUT_I32, int CG, bool PC = false>
+__global__ void __launch_bounds__(Cfg<BN, CG, PC>::kBlockThreads, 1)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
-    using C = Cfg<BN, CG>;
+    using C = Cfg<BN, CG, PC>;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B aligned base derived by pointer arithmetic on the __shared__ array, so the compiler keeps
     // the shared address space (LDS/STS, not generic LD/ST) for everything carved from it
@@ -595,7 +613,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
         // of slot x is visible through that release/acquire chain.
         const int j = (warp == 1) ? 0 : 1;
         if (j < C::kIssuers && rank == 0) {   // whole warp runs the loop (warp-uniform descriptors); one lane issues
-            const uint32_t idesc = idesc_i8(128 * CG, BN, /*a_signed=*/p.tx == nullptr);
+            const uint32_t idesc = idesc_i8(128 * CG, BN, /*a_signed=*/!PC && p.tx == nullptr);
             SegIter si(p, CG);
             int tile, s0, s1, cst = 0, it0 = 0;
             uint32_t cph = 0;
@@ -661,7 +679,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
         const int grp = (warp - 2) >> 2;              // steps it with it % kDeqGroups == grp
         const int r = q * 32 + lane;                  // weight row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        const bool signed_a = (p.tx == nullptr);   // no t_x: feed s8 lanes (XOR), else biased u8
+        const bool signed_a = !PC && (p.tx == nullptr);   // no t_x: feed s8 lanes (XOR), else biased u8
         const bool tw = (warp == 2 && lane == 0);
         SegIter si(p, CG);
         int tile, s0, s1, ws = 0, it = 0;
@@ -678,9 +696,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
                         if (t < nk && (!C::kDeqSplit || t == grp)) {
-                            const uint8_t* w = wb + t * kTileBytes;
-                            sc[t] = w[8192 + r];
-                            bias[t] = (128u - (uint32_t)w[8320 + r]) * 0x01010101u;
+                            const uint8_t* w = wb + t * C::kTB;
+                            if constexpr (PC) {          // lanes = q_u4: unpack only
+                                sc[t] = 1u;
+                                bias[t] = 0u;
+                            } else {
+                                sc[t] = w[8192 + r];
+                                bias[t] = (128u - (uint32_t)w[8320 + r]) * 0x01010101u;
+                            }
 #pragma unroll
                             for (int c = 0; c < 4; ++c) v[t][c] = *reinterpret_cast<const uint4*>(w + c * 2048 + r * 16);
                         }
@@ -765,9 +788,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                 const int m = m0 + jj;
                 // coherent (L2) loads: with the fused quantization they were written by this grid
                 sxs[jj] = (!OUT_I32 && m < p.M) ? __half2float(__ldcg(p.sx + m)) : 0.0f;
-                txs[jj] = (p.tx && m < p.M) ? 128 * __ldcg(p.tx + m) : 0;
+                txs[jj] = (p.tx && m < p.M) ? (PC ? 1 : 128) * __ldcg(p.tx + m) : 0;
             }
             float s0v[4] = {0.f, 0.f, 0.f, 0.f};
+            int z0v[4];
+            load_z4<PC>(p, n0 + 4 * l, z0v);
             if constexpr (!OUT_I32) {
                 const uint2 u = __ldg(reinterpret_cast<const uint2*>(p.s0 + n0 + 4 * l));
                 const __half2* h2 = reinterpret_cast<const __half2*>(&u);
@@ -810,6 +835,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                 // (w % nq is invariant): fetch their s0 now, off the critical path
                 const int nq = R / 4;
                 float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                int z4[4];
+                load_z4<PC>(p, n0 + crank * R + (et % nq) * 4, z4);
                 if constexpr (!OUT_I32) {
                     const uint2 u = __ldg(reinterpret_cast<const uint2*>(p.s0 + n0 + crank * R + (et % nq) * 4));
                     const __half2* h2 = reinterpret_cast<const __half2*>(&u);
@@ -855,7 +882,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
 #pragma unroll
                         for (int b = 0; b < kB; ++b) {
                             const int u = u0 + b, m = m0 + et / nq + step * u;
-                            if (et + 128 * u < items && m < p.M) write_out4<OUT_I32>(p, m, n, av[b], tv[b], sv[b], s4);
+                            if (et + 128 * u < items && m < p.M) write_out4<OUT_I32>(p, m, n, av[b], tv[b], sv[b], s4, z4);
                         }
                     }
                 }
@@ -913,7 +940,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
                         const int m = m0 + j0 + g + 4 * u;
-                        if (m < p.M && !(QOQ_ABLATE & 32)) write_out4<OUT_I32>(p, m, n0 + 4 * l, av[u], tv[u], sv[u], s0v);
+                        if (m < p.M && !(QOQ_ABLATE & 32)) write_out4<OUT_I32>(p, m, n0 + 4 * l, av[u], tv[u], sv[u], s0v, z0v);
                         else if ((QOQ_ABLATE & 32) && av[u].x == 0x7fffffff && sv[u] == 1.2345f) asm volatile("trap;");
                     }
                     if (et == 0 && ci == 0) QOQ_TRACE(p, 29);
@@ -943,7 +970,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG>::kBlockThreads, 1)
                         for (int u = 0; u < C::kFinU; ++u) {
                             const int jj = jb + g + 4 * u;
                             *reinterpret_cast<int4*>(wst + (size_t)jj * 128 + 4 * l) = make_int4(0, 0, 0, 0);
-                            if (m0 + jj < p.M) write_out4<OUT_I32>(p, m0 + jj, n0 + 4 * l, acc[u], txs[jj], sxs[jj], s0v);
+                            if (m0 + jj < p.M) write_out4<OUT_I32>(p, m0 + jj, n0 + 4 * l, acc[u], txs[jj], sxs[jj], s0v, z0v);
                         }
                     }
                     if (et == 0) {
@@ -1140,10 +1167,10 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     return p;
 }
 
-template <int BN, bool OUT_I32, int CG>
+template <int BN, bool OUT_I32, int CG, bool PC = false>
 static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t st, bool pdl) {
-    using C = Cfg<BN, CG>;
-    auto kern = w4a8_gemm_kernel<BN, OUT_I32, CG>;
+    using C = Cfg<BN, CG, PC>;
+    auto kern = w4a8_gemm_kernel<BN, OUT_I32, CG, PC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     auto enc = encode_fn();
@@ -1183,6 +1210,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     kp.ldx = a.ldx;
     kp.K = a.K;
     kp.qsync = a.qsync;
+    kp.zw = a.zw;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.G * CG);
     cfg.blockDim = dim3(C::kBlockThreads);
@@ -1209,6 +1237,10 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
 
 template <int BN>
 static cudaError_t launch_bn_cg(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl) {
+    if (a.zw) {   // per-channel W4A8: single-CTA tiles only
+        if (p.CG != 1) return cudaErrorInvalidValue;
+        return a.out_i32 ? launch_bn<BN, true, 1, true>(a, p, st, pdl) : launch_bn<BN, false, 1, true>(a, p, st, pdl);
+    }
     if (p.CG == 2) {
         if constexpr (BN >= 32)
             return a.out_i32 ? launch_bn<BN, true, 2>(a, p, st, pdl) : launch_bn<BN, false, 2>(a, p, st, pdl);

@@ -45,7 +45,7 @@ def test_library_is_sm100a_only(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert lib.qoq_abi_version() == 2
+    assert lib.qoq_abi_version() == 3
     for s in range(0, 8):
         assert lib.qoq_status_string(s)
 
@@ -90,3 +90,24 @@ def test_host_validation_before_any_device_work(lib):
     # M == 0 is a no-op that never touches the device
     assert lib.qoq_w4a8_gemm(fake, fake, None, fake, fake, 0, 256, 256, 128, fake, 256, None, 0, None) == 0
     assert lib.qoq_quantize_activations_per_token(fake, 0, 256, 256, fake, fake, None, None) == 0
+
+
+def test_per_channel_sizes_and_validation(lib):
+    """Per-channel W4A8 (NEXT-1): 8192-byte tiles; t_x and 4-byte-aligned z_w are required; shape
+    errors as the g128 calls — all host-side, before any device work."""
+    P = ctypes.c_void_p
+    fake = P(1 << 20)
+    assert lib.qoq_pc_packed_weight_bytes(256, 256) == 4 * 8192
+    assert lib.qoq_pc_packed_weight_bytes(4096, 14336) == 32 * 112 * 8192
+    assert lib.qoq_pc_packed_weight_bytes(100, 256) == 0
+    assert lib.qoq_pc_quantize_weights(fake, 200, 256, fake, 1 << 20, fake, fake, None) == 2
+    assert lib.qoq_pc_quantize_weights(fake, 256, 256, fake, 10, fake, fake, None) == 5
+    args = (fake, fake, None, fake, fake, fake, 4, 256, 256, fake, 256, None, 0, None)
+    assert lib.qoq_pc_w4a8_gemm(*args) == 1                                  # t_x missing
+    assert lib.qoq_pc_w4a8_gemm(fake, fake, fake, fake, fake, P((1 << 20) + 1), 4, 256, 256, fake, 256,
+                                None, 0, None) == 1                          # z_w misaligned
+    assert lib.qoq_pc_w4a8_gemm(fake, fake, fake, fake, fake, fake, 4, 256, 200, fake, 256,
+                                None, 0, None) == 2                          # K % 128
+    assert lib.qoq_pc_w4a8_gemm_i32(fake, None, fake, fake, 4, 256, 256, fake, 256, None, 0, None) == 1
+    assert lib.qoq_pc_w4a8_gemm(fake, fake, fake, fake, fake, fake, 0, 256, 256, fake, 256,
+                                None, 0, None) == 0                          # M == 0: no-op
