@@ -46,6 +46,11 @@ def gemm_bytes(M, N, K):
     return N * K // 2 + 2 * N * (K // 128) + 2 * N + M * K + 2 * M + 4 * M + 2 * M * N
 
 
+def pc_gemm_bytes(M, N, K):
+    """Per-channel W4A8 (NEXT-1): u4 codes + s_w + z_w + q_x + s_x + t_x + Y (no level-2 bytes)."""
+    return N * K // 2 + 2 * N + N + M * K + 2 * M + 4 * M + 2 * M * N
+
+
 def quant_bytes(M, K):
     """Per-token quantizer: read X fp16, write q_x, s_x, t_x."""
     return 2 * M * K + M * K + 2 * M + 4 * M
@@ -254,6 +259,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="per-projection GEMM breakdown and M sweep")
+    ap.add_argument("--no-per-channel", action="store_true",
+                    help="skip the per-channel W4A8 (NEXT-1) decode step measurement")
     ap.add_argument("--unfused-gate-up", action="store_true", help="run gate and up as two GEMMs")
     ap.add_argument("--fused-quant", action="store_true",
                     help="qoq_w4a8_linear per linear: per-token quantization fused into the GEMM prologue "
@@ -415,6 +422,11 @@ def main():
             "clocks": sampler.summary(), "roofline": roofline,
             "decode_tops": tops, "decode_frac_int8_datasheet": tops / INT8_DATASHEET_TOPS}
 
+    # ---- per-channel W4A8 (NEXT-1, §5.2.2): the same decode step on per-channel packed weights
+    if not args.no_per_channel and world == 1:
+        line["per_channel"] = per_channel_measure(qoq, torch, args, shapes, layers, dev, stream, X, quant_out,
+                                                  Ybuf, ws, timed)
+
     # ---- e2e through the C ABI with host buffers (H2D + quantize + GEMM + D2H per GEMM)
     if not args.no_e2e:
         line["e2e"] = e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes)
@@ -513,6 +525,53 @@ def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stre
             "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": steps, "streams": nstreams,
             "api": "qoq_linear_host (C ABI, pinned host X/Y) per GEMM, calls alternating over "
                    f"{nstreams} streams, the step captured as one CUDA graph"}
+
+
+def per_channel_measure(qoq, torch, args, shapes, layers, dev, stream, X, quant_out, Ybuf, ws, timed):
+    """The decode step with per-channel W4A8 weights (quantizer + qoq_pc_w4a8_gemm per projection),
+    captured as one CUDA graph like the main step; GB/s over the per-channel algorithmic bytes."""
+    M = args.M
+    gen = torch.Generator(device=dev)
+    pcs = []
+    with torch.cuda.stream(stream):
+        for l in range(layers):
+            row = []
+            for i, (name, N, K, kind, qg) in enumerate(shapes):
+                gen.manual_seed(1000 * l + 17 * i)
+                W = synth.device_weights_fp16(N, K, gen, dev)
+                row.append(qoq.pc_quantize_weights(W, stream=stream))
+                del W
+            pcs.append(row)
+    stream.synchronize()
+
+    def run():
+        for l in range(layers):
+            done = set()
+            for i, (name, N, K, kind, qg) in enumerate(shapes):
+                if qg not in done:
+                    qoq.quantize_activations_per_token(X[qg], out=quant_out[qg], stream=stream)
+                    done.add(qg)
+                qx, sx, tx = quant_out[qg]
+                p, s_w, z_w = pcs[l][i]
+                qoq.pc_w4a8_gemm(qx, sx, tx, p, s_w, z_w, N, out=Ybuf[name], workspace=ws, stream=stream)
+
+    with torch.cuda.stream(stream):
+        run()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            run()
+        steps = max(10, args.steps // 2)
+        ms = timed(g, steps, 3) / steps
+    b = 0
+    for name, N, K, kind, qg in shapes:
+        b += pc_gemm_bytes(M, N, K) * layers
+    shp = {n: (N, K) for n, N, K, _ in synth.MODELS[args.model][0]}
+    for src in ("qkv", "o", "gate", "down"):
+        b += quant_bytes(M, shp[src][1]) * layers
+    del pcs
+    return {"value": b / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "what": "same decode step, per-channel W4A8 weights (qoq_pc_w4a8_gemm, NEXT-1)"}
 
 
 def prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream):

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--time", action="store_true")
     ap.add_argument("--with-quant", action="store_true")
     ap.add_argument("--fused", action="store_true", help="qoq_w4a8_linear (quantization fused into the GEMM)")
+    ap.add_argument("--pc", action="store_true", help="per-channel W4A8 (qoq_pc_w4a8_gemm, NEXT-1)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     qoq.load()
@@ -36,7 +37,8 @@ def main():
     packs = []
     for l in range(a.layers):
         gen.manual_seed(l)
-        packs.append(qoq.quantize_weights(synth.device_weights_fp16(a.N, a.K, gen, dev)))
+        W = synth.device_weights_fp16(a.N, a.K, gen, dev)
+        packs.append(qoq.pc_quantize_weights(W) if a.pc else qoq.quantize_weights(W))
     X = synth.device_activations_fp16(a.M, a.K, gen, dev)
     q = qoq.quantize_activations_per_token(X)
     Y = torch.empty(a.M, a.N, dtype=torch.float16, device=dev)
@@ -44,7 +46,11 @@ def main():
     s = torch.cuda.Stream()
 
     def run():
-        for p, s0 in packs:
+        for pk in packs:
+            if a.pc:
+                qoq.pc_w4a8_gemm(*q, *pk, a.N, out=Y, workspace=ws, stream=s)
+                continue
+            p, s0 = pk
             if a.fused:
                 qoq.w4a8_linear(X, p, s0, a.N, out=Y, workspace=ws, stream=s)
                 continue
