@@ -63,6 +63,13 @@ def lib() -> ctypes.CDLL:
                 "oracle_pc_pack": (I, [P, I, I, P]),
                 "oracle_pc_unpack": (I, [P, I, I, P]),
                 "oracle_pc_gemm_i32": (I, [P, P, P, I, I, I, P]),
+                "oracle_d2h_rn": (ctypes.c_uint16, [ctypes.c_double]),
+                "oracle_rmsnorm_rinv": (ctypes.c_double, [P, I, ctypes.c_double]),
+                "oracle_rmsnorm_fp16": (I, [P, I, I, I, P, ctypes.c_double, P]),
+                "oracle_rmsnorm_quantize": (I, [P, I, I, I, P, ctypes.c_double, P, P, P]),
+                "oracle_silu_f64": (ctypes.c_double, [ctypes.c_double]),
+                "oracle_silu_mul_fp16": (I, [P, P, I, I, I, P]),
+                "oracle_silu_mul_quantize": (I, [P, P, I, I, I, P, P, P]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -282,3 +289,78 @@ def pc_gemm_i32(qx: np.ndarray, qu4: np.ndarray, z_w: np.ndarray) -> np.ndarray:
 
 def pc_acc_from_packed(qx: np.ndarray, packed: np.ndarray, z_w: np.ndarray, N: int, K: int) -> np.ndarray:
     return pc_gemm_i32(qx, pc_unpack(packed, N, K), z_w)
+
+
+# ---- NEXT-2: activation quantization fused into RMSNorm / SiLU·mul (Fig. 7; Q23-Q26) ----
+
+def d2h_rn(x: float) -> int:
+    """binary64 -> binary16 bits, one round-to-nearest-even (Q24)."""
+    return lib().oracle_d2h_rn(float(x))
+
+
+def rmsnorm_rinv(x: np.ndarray, eps: float) -> float:
+    """r = 1/sqrt(S/K + eps), S = exact Σx² rounded once to fp64 (Q25). x: one fp16 row."""
+    x = _u16(x)
+    return lib().oracle_rmsnorm_rinv(_p(x), x.shape[-1], float(eps))
+
+
+def rmsnorm_fp16(X: np.ndarray, gamma: np.ndarray, eps: float, K: int | None = None) -> np.ndarray:
+    """Llama RMSNorm output in fp16: fp16_rn((x·r)·γ) (Q23-Q25). X [M][ldx] -> [M][K]."""
+    X, gamma = _u16(X), _u16(gamma)
+    M, ldx = X.shape
+    K = ldx if K is None else K
+    Y = np.empty((M, K), np.uint16)
+    _check(lib().oracle_rmsnorm_fp16(_p(X), M, K, ldx, _p(gamma), float(eps), _p(Y)), "rmsnorm_fp16")
+    return Y.view(np.float16)
+
+
+def rmsnorm_quantize(X: np.ndarray, gamma: np.ndarray, eps: float, K: int | None = None):
+    """O4 of rmsnorm_fp16 (the fused layernorm + quantization of P:410) -> (qx, sx, tx)."""
+    X, gamma = _u16(X), _u16(gamma)
+    M, ldx = X.shape
+    K = ldx if K is None else K
+    qx = np.empty((M, K), np.int8)
+    sx = np.empty(M, np.uint16)
+    tx = np.empty(M, np.int32)
+    _check(lib().oracle_rmsnorm_quantize(_p(X), M, K, ldx, _p(gamma), float(eps), _p(qx), _p(sx), _p(tx)),
+           "rmsnorm_quantize")
+    return qx, sx.view(np.float16), tx
+
+
+def silu_f64(g: float) -> float:
+    """silu(g) = g / (1 + exp(-g)) in fp64 (Q26)."""
+    return lib().oracle_silu_f64(float(g))
+
+
+def _gate_up(G: np.ndarray, U: np.ndarray | None, K: int | None):
+    """(G, U) as two [M][K] arrays, or G = the [M][2K] gate_up output (gate | up) with U None."""
+    G = _u16(G)
+    if U is None:
+        M, ld = G.shape
+        K = ld // 2 if K is None else K
+        return G, G[:, K:].copy(), M, K
+    U = _u16(U)
+    M = G.shape[0]
+    K = G.shape[1] if K is None else K
+    return np.ascontiguousarray(G[:, :K]), np.ascontiguousarray(U[:, :K]), M, K
+
+
+def silu_mul_fp16(G: np.ndarray, U: np.ndarray | None = None, K: int | None = None) -> np.ndarray:
+    """fp16_rn(silu(g)·u) (Q24, Q26) -> [M][K] fp16."""
+    G, U, M, K = _gate_up(G, U, K)
+    G = np.ascontiguousarray(G[:, :K])
+    H = np.empty((M, K), np.uint16)
+    _check(lib().oracle_silu_mul_fp16(_p(G), _p(U), M, K, K, _p(H)), "silu_mul_fp16")
+    return H.view(np.float16)
+
+
+def silu_mul_quantize(G: np.ndarray, U: np.ndarray | None = None, K: int | None = None):
+    """O4 of silu_mul_fp16 (the fused activation + quantization of P:410) -> (qx, sx, tx)."""
+    G, U, M, K = _gate_up(G, U, K)
+    G = np.ascontiguousarray(G[:, :K])
+    qx = np.empty((M, K), np.int8)
+    sx = np.empty(M, np.uint16)
+    tx = np.empty(M, np.int32)
+    _check(lib().oracle_silu_mul_quantize(_p(G), _p(U), M, K, K, _p(qx), _p(sx), _p(tx)),
+           "silu_mul_quantize")
+    return qx, sx.view(np.float16), tx

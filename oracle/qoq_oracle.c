@@ -42,10 +42,11 @@ float oracle_h2f(uint16_t h) {
     return sign ? -v : v;
 }
 
-uint16_t oracle_f2h_rn(float f) {
+/* binary64 -> binary16, round to nearest, ties to even (one rounding; Q8, Q10, Q24). */
+uint16_t oracle_d2h_rn(double f) {
     uint16_t sign = signbit(f) ? 0x8000 : 0;
     if (isnan(f)) return 0x7e00;
-    double a = fabs((double)f);
+    double a = fabs(f);
     if (a == 0.0) return sign;
     if (isinf(a)) return sign | 0x7c00;
     int E;
@@ -62,6 +63,9 @@ uint16_t oracle_f2h_rn(float f) {
     int man = (int)(ldexp(v, -e) * 1024.0) - 1024;
     return sign | (uint16_t)((e + 15) << 10) | (uint16_t)man;
 }
+
+/* binary32 -> binary16: every float is exactly a double, so one rounding of that double. */
+uint16_t oracle_f2h_rn(float f) { return oracle_d2h_rn((double)f); }
 
 /* Q1: ⌈·⌋ = round half away from zero; exact integer form for a/b, b > 0. */
 int oracle_rhai(int a, int b) {
@@ -373,4 +377,73 @@ int oracle_pc_gemm_i32(const int8_t* qx, const uint8_t* qu4, const uint8_t* z_w,
             acc[(size_t)m * N + n] = (int32_t)s;
         }
     return overflow ? -2 : 0;
+}
+
+/* ---------------- NEXT-2: activation quantization fused into RMSNorm / SiLU·mul (Fig. 7) ----
+ * The fused kernels are defined as the composition "fp16 output of the layer, then O4", so these
+ * oracles compute the fp16 layer output and call oracle_quantize_activations on it (Q23). */
+
+/* Q25: S = Σ_k x_k^2 exactly (each x^2 of an fp16 x is an integer multiple of 2^-48 below 2^32, so
+ * Σ x^2 * 2^48 is an integer < 2^95 for K < 2^31: a 128-bit integer sum), rounded ONCE to fp64;
+ * then r = 1 / sqrt(S / K + eps) in IEEE fp64 (each operation correctly rounded). S / K + eps == 0
+ * (all-zero row, eps == 0) gives r = 0. */
+double oracle_rmsnorm_rinv(const uint16_t* x, int K, double eps) {
+    unsigned __int128 S = 0;
+    for (int k = 0; k < K; ++k) {
+        double v = (double)oracle_h2f(x[k]);
+        S += (unsigned __int128)ldexp(v * v, 48);   /* v*v exact (22 bits); integer-valued */
+    }
+    double ms = ldexp((double)S, -48) / (double)K + eps;
+    return ms == 0.0 ? 0.0 : 1.0 / sqrt(ms);
+}
+
+/* RMSNorm (Llama form, Q23): y[m][k] = fp16_rn( (x[m][k] * r_m) * gamma[k] ), products in fp64,
+ * left to right, one rounding to fp16 (Q24). X [M][ldx], gamma [K], Y [M][K] (fp16 bits). */
+int oracle_rmsnorm_fp16(const uint16_t* X, int M, int K, int ldx, const uint16_t* gamma, double eps,
+                        uint16_t* Y) {
+    if (M < 0 || K <= 0 || ldx < K || eps < 0.0) return -1;
+    for (int m = 0; m < M; ++m) {
+        const uint16_t* x = X + (size_t)m * ldx;
+        double r = oracle_rmsnorm_rinv(x, K, eps);
+        for (int k = 0; k < K; ++k)
+            Y[(size_t)m * K + k] = oracle_d2h_rn((double)oracle_h2f(x[k]) * r * (double)oracle_h2f(gamma[k]));
+    }
+    return 0;
+}
+
+int oracle_rmsnorm_quantize(const uint16_t* X, int M, int K, int ldx, const uint16_t* gamma, double eps,
+                            int8_t* qx, uint16_t* sx, int32_t* tx) {
+    if (M < 0 || K <= 0 || ldx < K || eps < 0.0) return -1;
+    uint16_t* Y = (uint16_t*)malloc((size_t)(M > 0 ? M : 1) * K * sizeof(uint16_t));
+    if (!Y) return -3;
+    int rc = oracle_rmsnorm_fp16(X, M, K, ldx, gamma, eps, Y);
+    if (!rc) rc = oracle_quantize_activations(Y, M, K, K, qx, sx, tx);
+    free(Y);
+    return rc;
+}
+
+/* SiLU (Llama FFN activation, Q26): silu(g) = g / (1 + exp(-g)) in fp64. */
+double oracle_silu_f64(double g) { return g / (1.0 + exp(-g)); }
+
+/* h[m][k] = fp16_rn( silu(g[m][k]) * u[m][k] ) in fp64 (Q24, Q26). G, U: [M][ldg]. H: [M][K]. */
+int oracle_silu_mul_fp16(const uint16_t* G, const uint16_t* U, int M, int K, int ldg, uint16_t* H) {
+    if (M < 0 || K <= 0 || ldg < K) return -1;
+    for (int m = 0; m < M; ++m)
+        for (int k = 0; k < K; ++k) {
+            double g = (double)oracle_h2f(G[(size_t)m * ldg + k]);
+            double u = (double)oracle_h2f(U[(size_t)m * ldg + k]);
+            H[(size_t)m * K + k] = oracle_d2h_rn(oracle_silu_f64(g) * u);
+        }
+    return 0;
+}
+
+int oracle_silu_mul_quantize(const uint16_t* G, const uint16_t* U, int M, int K, int ldg,
+                             int8_t* qx, uint16_t* sx, int32_t* tx) {
+    if (M < 0 || K <= 0 || ldg < K) return -1;
+    uint16_t* H = (uint16_t*)malloc((size_t)(M > 0 ? M : 1) * K * sizeof(uint16_t));
+    if (!H) return -3;
+    int rc = oracle_silu_mul_fp16(G, U, M, K, ldg, H);
+    if (!rc) rc = oracle_quantize_activations(H, M, K, K, qx, sx, tx);
+    free(H);
+    return rc;
 }

@@ -6,7 +6,7 @@
  * shares no code, header, table or constant generator with it.
  *
  * Citations: "P:n" = line n of the paper's LaTeX source, with its section/equation.
- * Readings of silent/ambiguous passages are numbered Q1..Q19 as in DESIGN.md §3.
+ * Readings of silent/ambiguous passages are numbered Q1..Q26 as in DESIGN.md §3.
  *
  * fp16 values are carried as raw IEEE binary16 bit patterns (uint16_t).
  * All functions return 0 on success, a negative value on a precondition failure.
@@ -23,6 +23,7 @@ extern "C" {
 /* IEEE binary16 <-> binary32. f2h rounds to nearest, ties to even (Q8, Q10). */
 float    oracle_h2f(uint16_t h);
 uint16_t oracle_f2h_rn(float f);
+uint16_t oracle_d2h_rn(double f);   /* binary64 -> binary16, one RNE rounding (Q24) */
 
 /* Round half away from zero of the integer quotient a/b, b > 0 (Q1: the paper's ⌈·⌋). */
 int      oracle_rhai(int a, int b);
@@ -103,6 +104,29 @@ int oracle_pc_unpack(const uint8_t* packed, int N, int K, uint8_t* qu4);
  * The epilogue reference is oracle_epilogue_f64(acc, s_x, s_w): y = acc * s_x[m] * s_w[n]. */
 int oracle_pc_gemm_i32(const int8_t* qx, const uint8_t* qu4, const uint8_t* z_w, int M, int N, int K,
                        int32_t* acc);
+
+/* ---------------- NEXT-2: fused activation quantization (Fig. 7) ----------------
+ * "we fuse activation quantization into the preceding layernorm for the QKV projection and the first
+ * FFN layer, or into the preceding activation kernel for the second FFN layer". The paper
+ * does not define the layers; readings Q23-Q26: Llama RMSNorm and SiLU·mul, the fp16
+ * layer output rounded once from fp64, then O4 on it (fused == unfused composition, bit for bit). */
+
+/* r = 1 / sqrt(S/K + eps), S = Σ x^2 summed exactly and rounded once to fp64 (Q25); 0 if S/K+eps==0. */
+double oracle_rmsnorm_rinv(const uint16_t* x, int K, double eps);
+/* Y[m][k] = fp16_rn((x[m][k] * r_m) * gamma[k]) in fp64. X [M][ldx], gamma [K], Y [M][K]. */
+int oracle_rmsnorm_fp16(const uint16_t* X, int M, int K, int ldx, const uint16_t* gamma, double eps,
+                        uint16_t* Y);
+/* O4 of oracle_rmsnorm_fp16's output: qx [M][K], sx [M], tx [M] (nullable). */
+int oracle_rmsnorm_quantize(const uint16_t* X, int M, int K, int ldx, const uint16_t* gamma, double eps,
+                            int8_t* qx, uint16_t* sx, int32_t* tx);
+/* silu(g) = g / (1 + exp(-g)) in fp64 (Q26). */
+double oracle_silu_f64(double g);
+/* H[m][k] = fp16_rn(silu(G[m][k]) * U[m][k]) in fp64. G, U [M][ldg] (e.g. the two halves of the
+ * fused gate_up output, ldg = 2K), H [M][K]. */
+int oracle_silu_mul_fp16(const uint16_t* G, const uint16_t* U, int M, int K, int ldg, uint16_t* H);
+/* O4 of oracle_silu_mul_fp16's output. */
+int oracle_silu_mul_quantize(const uint16_t* G, const uint16_t* U, int M, int K, int ldg,
+                             int8_t* qx, uint16_t* sx, int32_t* tx);
 
 /* Number of OpenMP threads the oracle's parallel loops use (1 without OpenMP). */
 int oracle_num_threads(void);
