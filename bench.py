@@ -56,6 +56,16 @@ def quant_bytes(M, K):
     return 2 * M * K + M * K + 2 * M + 4 * M
 
 
+def rmsnorm_quant_bytes(M, K):
+    """RMSNorm + per-token quantizer fused (NEXT-2): read X fp16 and gamma, write q_x, s_x, t_x."""
+    return 2 * M * K + 2 * K + M * K + 2 * M + 4 * M
+
+
+def silu_quant_bytes(M, I):
+    """SiLU(gate)·up + per-token quantizer fused (NEXT-2): read gate and up fp16, write q_x, s_x, t_x."""
+    return 4 * M * I + M * I + 2 * M + 4 * M
+
+
 def gemm_ops(M, N, K):
     return 2 * M * N * K
 
@@ -256,6 +266,7 @@ def main():
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--prefill-M", type=int, default=4096)
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-fused-block", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="per-projection GEMM breakdown and M sweep")
@@ -427,6 +438,11 @@ def main():
         line["per_channel"] = per_channel_measure(qoq, torch, args, shapes, layers, dev, stream, X, quant_out,
                                                   Ybuf, ws, timed)
 
+    # ---- the paper's block mapping (Fig. 7): quantization fused into RMSNorm / SiLU·mul (NEXT-2)
+    if not args.no_fused_block and world == 1:
+        line["fused_block"] = fused_block_measure(qoq, torch, args, shapes, packed, layers, dev, stream, X,
+                                                  quant_out, Ybuf, ws, timed)
+
     # ---- e2e through the C ABI with host buffers (H2D + quantize + GEMM + D2H per GEMM)
     if not args.no_e2e:
         line["e2e"] = e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes)
@@ -572,6 +588,88 @@ def per_channel_measure(qoq, torch, args, shapes, layers, dev, stream, X, quant_
     del pcs
     return {"value": b / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
             "what": "same decode step, per-channel W4A8 weights (qoq_pc_w4a8_gemm, NEXT-1)"}
+
+
+def fused_block_measure(qoq, torch, args, shapes, packed, layers, dev, stream, X, quant_out, Ybuf, ws, timed):
+    """The decode step with the activation quantization of Fig. 7: RMSNorm+quantize before qkv
+    and gate_up, the separate quantizer before o, SiLU·mul+quantize (on the gate_up GEMM's own output)
+    before down — one CUDA graph; plus each fused quantizer timed alone at decode M and prefill M
+    (inputs rotated over > L2 bytes) against the HBM peak."""
+    M = args.M
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(23)
+    Kh = {qg: K for _, N, K, _, qg in shapes}
+    I = Kh["mlp_act"]
+    gam = [(1.0 + 0.1 * torch.randn(2, Kh["attn_in"], generator=gen, device=dev)).half() for _ in range(layers)]
+    eps = 1e-5
+
+    def run():
+        n = 0
+        for l in range(layers):
+            for i, (name, N, K, kind, qg) in enumerate(shapes):
+                if qg == "attn_in":
+                    qoq.rmsnorm_quantize(X[qg], gam[l][0], eps, out=quant_out[qg], stream=stream)
+                elif qg == "mlp_in":
+                    qoq.rmsnorm_quantize(X[qg], gam[l][1], eps, out=quant_out[qg], stream=stream)
+                elif qg == "mlp_act":
+                    qoq.silu_mul_quantize(Ybuf["gate_up"], out=quant_out[qg], stream=stream)
+                else:
+                    qoq.quantize_activations_per_token(X[qg], out=quant_out[qg], stream=stream)
+                qx, sx, tx = quant_out[qg]
+                p, s0 = packed[l][i]
+                qoq.w4a8_gemm(qx, sx, tx, p, s0, N, out=Ybuf[name], workspace=ws, stream=stream)
+                n += 2
+        return n
+
+    with torch.cuda.stream(stream):
+        run()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            launches = run()
+        steps = max(10, args.steps // 2)
+        ms = timed(g, steps, 3) / steps
+    b = sum(gemm_bytes(M, N, K) for _, N, K, _, _ in shapes) * layers
+    b += (2 * rmsnorm_quant_bytes(M, Kh["attn_in"]) + quant_bytes(M, Kh["attn_out"]) + silu_quant_bytes(M, I)) * layers
+    out = {"value": b / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
+           "launches_per_step": launches,
+           "what": "decode step with Fig. 7's quantization mapping: rmsnorm_quantize -> qkv, quantize -> o, "
+                   "rmsnorm_quantize -> gate_up, silu_mul_quantize(gate_up output) -> down (NEXT-2)"}
+    peak, _ = load_peaks()
+    kern = {}
+    for Mk in (M, args.prefill_M):
+        for kname, K, nbytes in (("rmsnorm_quant_kernel", Kh["attn_in"], rmsnorm_quant_bytes(Mk, Kh["attn_in"])),
+                                 ("silu_mul_quant_kernel", I, silu_quant_bytes(Mk, I))):
+            in_bytes = (2 if kname.startswith("rms") else 4) * Mk * K
+            nbuf = max(1, min(8, -(-256 * 2 ** 20 // in_bytes)))     # rotate inputs over >= 256 MB (> L2)
+            if kname.startswith("rms"):
+                ins = [synth.device_activations_fp16(Mk, K, gen, dev) for _ in range(nbuf)]
+            else:
+                ins = [(2.0 * torch.randn(Mk, 2 * K, generator=gen, device=dev)).half() for _ in range(nbuf)]
+            o = (torch.empty(Mk, K, dtype=torch.int8, device=dev), torch.empty(Mk, dtype=torch.float16, device=dev),
+                 torch.empty(Mk, dtype=torch.int32, device=dev))
+            reps = 4 * nbuf if Mk > M else 64
+
+            def krun():
+                for r in range(reps):
+                    if kname.startswith("rms"):
+                        qoq.rmsnorm_quantize(ins[r % nbuf], gam[0][0], eps, out=o, stream=stream)
+                    else:
+                        qoq.silu_mul_quantize(ins[r % nbuf], out=o, stream=stream)
+
+            with torch.cuda.stream(stream):
+                krun()
+                stream.synchronize()
+                gk = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gk, stream=stream):
+                    krun()
+                us = timed(gk, 5, 2) / 5 / reps * 1e3
+            kern[f"{kname}_M{Mk}"] = {"K": K, "us": us, "GBps": nbytes / (us * 1e-6) / 1e9,
+                                      "frac_hbm": nbytes / (us * 1e-6) / 1e9 / peak,
+                                      "algorithmic_bytes": nbytes}
+            del ins, o
+    out["kernels"] = kern
+    return out
 
 
 def prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream):

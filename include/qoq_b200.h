@@ -40,7 +40,7 @@ typedef enum {
 const char* qoq_status_string(int status);
 /* ABI version of this header (incremented on any signature or layout change). */
 int qoq_abi_version(void);
-#define QOQ_ABI_VERSION 3
+#define QOQ_ABI_VERSION 4
 
 /* ----------------------------------------------------------------------------------------------
  * Packed weight layout (frozen). The B200 form of "store the weights in the order
@@ -160,8 +160,30 @@ int qoq_pc_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed
                          int M, int N, int K, int32_t* acc, int ldacc,
                          void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Activation quantization fused into the producing layer (NEXT-2) ----
+ * P:410 (§5.1, Fig. 7): "we fuse activation quantization into the preceding layernorm for
+ * the QKV projection and the first FFN layer, or into the preceding activation kernel for the second
+ * FFN layer". Each call writes exactly what qoq_quantize_activations_per_token would write for the
+ * layer's fp16 output (Q23), without that output being stored:
+ *
+ * qoq_rmsnorm_quantize — Llama RMSNorm before qkv / gate_up (Q23-Q25):
+ *   y[m][k] = fp16_rn((x[m][k] · r_m) · gamma[k]) in fp64, r_m = 1 / sqrt(S_m / K + eps) in fp64,
+ *   S_m = Σ_k x[m][k]² summed EXACTLY and rounded once (r is independent of reduction order);
+ *   S_m / K + eps == 0 gives r_m = 0. Then q_x, s_x, t_x of y as in the per-token quantizer.
+ *   X_fp16 [M][ldx] (ldx >= K, ldx % 8 == 0), gamma_fp16 [K], eps >= 0 finite (Llama: 1e-5).
+ * qoq_silu_mul_quantize — the FFN activation before down (Q24, Q26):
+ *   h[m][k] = fp16_rn(silu(g) · u), silu(g) = g / (1 + exp(-g)) in fp64, g = gate[m][k], u = up[m][k];
+ *   gate_fp16 / up_fp16 [M][ldg] (e.g. the fused gate_up GEMM output: up = gate + K, ldg = 2K).
+ * Outputs (both): qx [M][K] int8 (8-byte aligned), sx_fp16 [M], tx [M] int32 row sums (nullable).
+ * Requires K % 8 == 0, 16-byte aligned fp16 inputs. M == 0 is a no-op. Errors as
+ * qoq_quantize_activations_per_token (QOQ_ERR_INVALID_ARG also for a negative / non-finite eps). */
+int qoq_rmsnorm_quantize(const void* X_fp16, int ldx, const void* gamma_fp16, double eps, int M, int K,
+                         int8_t* qx, void* sx_fp16, int32_t* tx, void* stream);
+int qoq_silu_mul_quantize(const void* gate_fp16, const void* up_fp16, int ldg, int M, int K,
+                          int8_t* qx, void* sx_fp16, int32_t* tx, void* stream);
+
 /* Kernels launched per successful call (launch accounting for benchmarks):
- * quantize_weights 2, quantize_activations_per_token 1, w4a8_gemm 1, w4a8_gemm_i32 1,
+ * quantize_weights 2, quantize_activations_per_token 1, rmsnorm_quantize 1, silu_mul_quantize 1, w4a8_gemm 1, w4a8_gemm_i32 1,
  * pc_quantize_weights 2, pc_w4a8_gemm 1, pc_w4a8_gemm_i32 1,
  * w4a8_linear 2 (1 when fused: QOQ_LINEAR_FUSED=1 and M <= 64), linear_host as w4a8_linear
  * (plus 2 async copies). */

@@ -23,10 +23,11 @@ LIB_PATH = os.path.join(_HERE, "libqoq_b200.so" if not os.environ.get("QOQ_LIB_V
                         else f"libqoq_b200_{os.environ['QOQ_LIB_VARIANT']}.so")
 GROUP = 128
 TILE_BYTES = 8448
-ABI_VERSION = 3
+ABI_VERSION = 4
 # kernels launched per call (matches include/qoq_b200.h)
 LAUNCHES = {"quantize_weights": 2, "quantize_activations_per_token": 1, "w4a8_gemm": 1,
-            "w4a8_gemm_i32": 1, "pc_quantize_weights": 2, "pc_w4a8_gemm": 1, "pc_w4a8_gemm_i32": 1}
+            "w4a8_gemm_i32": 1, "pc_quantize_weights": 2, "pc_w4a8_gemm": 1, "pc_w4a8_gemm_i32": 1,
+            "rmsnorm_quantize": 1, "silu_mul_quantize": 1}
 FUSE_MAX_M = 64   # w4a8_linear / linear_host with QOQ_LINEAR_FUSED=1: one fused kernel up to this M
 
 
@@ -76,6 +77,8 @@ def load() -> ctypes.CDLL:
             "qoq_pc_quantize_weights": (I, [P, I, I, P, Z, P, P, P]),
             "qoq_pc_w4a8_gemm": (I, [P, P, P, P, P, P, I, I, I, P, I, P, Z, P]),
             "qoq_pc_w4a8_gemm_i32": (I, [P, P, P, P, I, I, I, P, I, P, Z, P]),
+            "qoq_rmsnorm_quantize": (I, [P, I, P, ctypes.c_double, I, I, P, P, P, P]),
+            "qoq_silu_mul_quantize": (I, [P, P, I, I, I, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -169,6 +172,47 @@ def quantize_activations_per_token(X: torch.Tensor, K: int | None = None, want_t
     _check("qoq_quantize_activations_per_token",
            load().qoq_quantize_activations_per_token(_ptr(X), M, K, ldx, _ptr(qx), _ptr(sx), _ptr(tx),
                                                      _stream(stream)))
+    return qx, sx, tx
+
+
+def _act_out(M: int, K: int, device, want_tx: bool, out):
+    if out is not None:
+        return out
+    return (torch.empty(M, K, dtype=torch.int8, device=device),
+            torch.empty(M, dtype=torch.float16, device=device),
+            torch.empty(M, dtype=torch.int32, device=device) if want_tx else None)
+
+
+def rmsnorm_quantize(X: torch.Tensor, gamma: torch.Tensor, eps: float = 1e-5, K: int | None = None,
+                     want_tx: bool = True, out=None, stream=None):
+    """RMSNorm with the per-token INT8 quantization fused in (NEXT-2; C-ABI
+    qoq_rmsnorm_quantize): X [M][ldx] fp16, gamma [K] fp16 -> (qx int8 [M][K], sx fp16 [M], tx)."""
+    if X.dtype != torch.float16 or X.dim() != 2 or gamma.dtype != torch.float16:
+        raise ValueError("X must be a 2-D fp16 tensor and gamma fp16")
+    M, ldx = X.shape
+    K = ldx if K is None else K
+    qx, sx, tx = _act_out(M, K, X.device, want_tx, out)
+    _check("qoq_rmsnorm_quantize",
+           load().qoq_rmsnorm_quantize(_ptr(X), ldx, _ptr(gamma), float(eps), M, K, _ptr(qx), _ptr(sx),
+                                       _ptr(tx), _stream(stream)))
+    return qx, sx, tx
+
+
+def silu_mul_quantize(gate_up: torch.Tensor, K: int | None = None, want_tx: bool = True, out=None,
+                      stream=None):
+    """SiLU(gate)·up with the per-token INT8 quantization fused in (NEXT-2; C-ABI
+    qoq_silu_mul_quantize). gate_up [M][2K] fp16 is the fused gate_up GEMM output (gate | up)."""
+    if gate_up.dtype != torch.float16 or gate_up.dim() != 2:
+        raise ValueError("gate_up must be a 2-D fp16 tensor")
+    M, ld = gate_up.shape
+    K = ld // 2 if K is None else K
+    if not gate_up.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    qx, sx, tx = _act_out(M, K, gate_up.device, want_tx, out)
+    base = gate_up.data_ptr()
+    _check("qoq_silu_mul_quantize",
+           load().qoq_silu_mul_quantize(ctypes.c_void_p(base), ctypes.c_void_p(base + 2 * K), ld, M, K,
+                                        _ptr(qx), _ptr(sx), _ptr(tx), _stream(stream)))
     return qx, sx, tx
 
 

@@ -171,6 +171,32 @@ int qoq_quantize_activations_per_token(const void* X, int M, int K, int ldx, int
                    cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
 }
 
+int qoq_rmsnorm_quantize(const void* X, int ldx, const void* gamma, double eps, int M, int K, int8_t* qx,
+                         void* sx, int32_t* tx, void* stream) {
+    if (M < 0 || K <= 0 || ldx < K || !(eps >= 0.0) || eps > 1e300) return QOQ_ERR_INVALID_ARG;
+    if (K % 8 || ldx % 8) return QOQ_ERR_SHAPE;
+    if (M == 0) return QOQ_OK;
+    if (!X || !gamma || !qx || !sx || !aligned16(X) || !aligned16(gamma) || (reinterpret_cast<uintptr_t>(qx) & 7u))
+        return QOQ_ERR_INVALID_ARG;
+    int rc = check_arch(nullptr);
+    if (rc) return rc;
+    return launch_rmsnorm_quantize(X, ldx, gamma, eps, M, K, qx, sx, tx, static_cast<cudaStream_t>(stream), true) ==
+                   cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
+int qoq_silu_mul_quantize(const void* gate, const void* up, int ldg, int M, int K, int8_t* qx, void* sx,
+                          int32_t* tx, void* stream) {
+    if (M < 0 || K <= 0 || ldg < K) return QOQ_ERR_INVALID_ARG;
+    if (K % 8 || ldg % 8) return QOQ_ERR_SHAPE;
+    if (M == 0) return QOQ_OK;
+    if (!gate || !up || !qx || !sx || !aligned16(gate) || !aligned16(up) || (reinterpret_cast<uintptr_t>(qx) & 7u))
+        return QOQ_ERR_INVALID_ARG;
+    int rc = check_arch(nullptr);
+    if (rc) return rc;
+    return launch_silu_mul_quantize(gate, up, ldg, M, K, qx, sx, tx, static_cast<cudaStream_t>(stream), true) ==
+                   cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
 size_t qoq_gemm_workspace_bytes(int M, int N, int K) {
     if (gemm_shape_status(M, N, K, 128) != QOQ_OK || M == 0) return 0;
     return plan_gemm(M, N, K, num_sms_or_default()).ws_bytes;

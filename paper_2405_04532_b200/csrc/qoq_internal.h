@@ -61,4 +61,10 @@ cudaError_t launch_pc_quantize_weights(const void* W, int N, int K, void* packed
 cudaError_t launch_quantize_activations(const void* X, int M, int K, int ldx, int8_t* qx, void* sx,
                                         int32_t* tx, cudaStream_t st, bool pdl);
 
+// NEXT-2: per-token quantization fused into RMSNorm / SiLU·mul (fused_quant.cu)
+cudaError_t launch_rmsnorm_quantize(const void* X, int ldx, const void* gamma, double eps, int M, int K,
+                                    int8_t* qx, void* sx, int32_t* tx, cudaStream_t st, bool pdl);
+cudaError_t launch_silu_mul_quantize(const void* G, const void* U, int ldg, int M, int K, int8_t* qx, void* sx,
+                                     int32_t* tx, cudaStream_t st, bool pdl);
+
 }  // namespace qoq

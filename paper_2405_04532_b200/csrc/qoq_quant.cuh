@@ -9,6 +9,33 @@
 
 namespace qoq {
 
+// Block-wide max of non-negative values / int sum over a 1-D CTA (valid in every thread).
+__device__ __forceinline__ float block_reduce_max(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    v = (l < nw) ? red[l] : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;  // valid in every thread
+}
+
+__device__ __forceinline__ int block_reduce_sum(int v, int* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    v = (l < nw) ? red[l] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 // Symmetric fp16 scale: fp16_rn(amax / qmax); 1.0 for amax == 0; 2^-24 if it underflows to 0.
 __device__ __forceinline__ __half sym_scale(float amax, float qmax) {
     if (amax == 0.0f) return __float2half_rn(1.0f);

@@ -20,19 +20,6 @@
 
 namespace qoq {
 
-__device__ __forceinline__ float block_reduce_max(float v, float* red) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    v = (l < nw) ? red[l] : 0.0f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;  // valid in every thread
-}
-
 // block max of arbitrary-sign values (identity -inf; block_reduce_max above assumes v >= 0)
 __device__ __forceinline__ float block_reduce_max_signed(float v, float* red) {
     const float ninf = -__int_as_float(0x7f800000);
@@ -46,19 +33,6 @@ __device__ __forceinline__ float block_reduce_max_signed(float v, float* red) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;  // valid in every thread
-}
-
-__device__ __forceinline__ int block_reduce_sum(int v, int* red) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    v = (l < nw) ? red[l] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
 }
 
 // ------------------------------------------------------------------ weights, level 1

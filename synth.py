@@ -99,6 +99,16 @@ def fuse_gate_up(shapes):
     return out
 
 
+def rmsnorm_weight_fp16(K: int, seed: int = 0) -> np.ndarray:
+    """RMSNorm gain gamma[K] fp16 ~ 1 + 0.1 N(0,1) (NEXT-2 inputs; trained gains are O(1))."""
+    return (1.0 + 0.1 * normal(seed, 3, K)).astype(np.float16)
+
+
+def gate_up_fp16(M: int, K: int, seed: int = 0, scale: float = 2.0) -> np.ndarray:
+    """The fused gate_up GEMM output [M][2K] fp16 (gate | up) ~ N(0, scale^2): the SiLU·mul input."""
+    return (normal(seed, 4, M * 2 * K).reshape(M, 2 * K) * scale).astype(np.float16)
+
+
 # ---- device-side generators for the large benchmark stacks (torch's seeded Philox on the GPU;
 # same distributions as above; used by bench.py only, never as oracle inputs).
 

@@ -45,7 +45,7 @@ def test_library_is_sm100a_only(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert lib.qoq_abi_version() == 3
+    assert lib.qoq_abi_version() == 4
     for s in range(0, 8):
         assert lib.qoq_status_string(s)
 
@@ -111,3 +111,21 @@ def test_per_channel_sizes_and_validation(lib):
     assert lib.qoq_pc_w4a8_gemm_i32(fake, None, fake, fake, 4, 256, 256, fake, 256, None, 0, None) == 1
     assert lib.qoq_pc_w4a8_gemm(fake, fake, fake, fake, fake, fake, 0, 256, 256, fake, 256,
                                 None, 0, None) == 0                          # M == 0: no-op
+
+
+def test_fused_quantizer_validation(lib):
+    """NEXT-2 entries (qoq_rmsnorm_quantize, qoq_silu_mul_quantize): shape / eps / alignment errors
+    and the M == 0 no-op, all host-side, before any device work."""
+    P, D = ctypes.c_void_p, ctypes.c_double
+    fake = P(1 << 20)
+    assert lib.qoq_rmsnorm_quantize(fake, 256, fake, D(1e-5), 4, 204, fake, fake, None, None) == 2   # K % 8
+    assert lib.qoq_rmsnorm_quantize(fake, 128, fake, D(1e-5), 4, 256, fake, fake, None, None) == 1   # ldx < K
+    assert lib.qoq_rmsnorm_quantize(fake, 256, fake, D(-1.0), 4, 256, fake, fake, None, None) == 1   # eps < 0
+    assert lib.qoq_rmsnorm_quantize(fake, 256, fake, D(float("nan")), 4, 256, fake, fake, None, None) == 1
+    assert lib.qoq_rmsnorm_quantize(fake, 256, P((1 << 20) + 8), D(1e-5), 4, 256, fake, fake, None, None) == 1
+    assert lib.qoq_rmsnorm_quantize(fake, 256, fake, D(1e-5), 0, 256, fake, fake, None, None) == 0
+    assert lib.qoq_silu_mul_quantize(fake, fake, 512, 4, 252, fake, fake, None, None) == 2
+    assert lib.qoq_silu_mul_quantize(fake, fake, 128, 4, 256, fake, fake, None, None) == 1
+    assert lib.qoq_silu_mul_quantize(fake, P((1 << 20) + 2), 512, 4, 256, fake, fake, None, None) == 1
+    assert lib.qoq_silu_mul_quantize(fake, None, 512, 4, 256, fake, fake, None, None) == 1
+    assert lib.qoq_silu_mul_quantize(fake, fake, 512, 0, 256, fake, fake, None, None) == 0
