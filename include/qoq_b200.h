@@ -170,7 +170,7 @@ int qoq_pc_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed
  *   y[m][k] = fp16_rn((x[m][k] · r_m) · gamma[k]) in fp64, r_m = 1 / sqrt(S_m / K + eps) in fp64,
  *   S_m = Σ_k x[m][k]² summed EXACTLY and rounded once (r is independent of reduction order);
  *   S_m / K + eps == 0 gives r_m = 0. Then q_x, s_x, t_x of y as in the per-token quantizer.
- *   X_fp16 [M][ldx] (ldx >= K, ldx % 8 == 0), gamma_fp16 [K], eps >= 0 finite (Llama: 1e-5).
+ *   X_fp16 [M][ldx] (ldx >= K, ldx % 8 == 0), gamma_fp16 [K], eps >= 0 finite (Llama: 1e-5); K <= 65536.
  * qoq_silu_mul_quantize — the FFN activation before down (Q24, Q26):
  *   h[m][k] = fp16_rn(silu(g) · u), silu(g) = g / (1 + exp(-g)) in fp64, g = gate[m][k], u = up[m][k];
  *   gate_fp16 / up_fp16 [M][ldg] (e.g. the fused gate_up GEMM output: up = gate + K, ldg = 2K).

@@ -173,7 +173,7 @@ int qoq_quantize_activations_per_token(const void* X, int M, int K, int ldx, int
 
 int qoq_rmsnorm_quantize(const void* X, int ldx, const void* gamma, double eps, int M, int K, int8_t* qx,
                          void* sx, int32_t* tx, void* stream) {
-    if (M < 0 || K <= 0 || ldx < K || !(eps >= 0.0) || eps > 1e300) return QOQ_ERR_INVALID_ARG;
+    if (M < 0 || K <= 0 || K > 65536 || ldx < K || !(eps >= 0.0) || eps > 1e300) return QOQ_ERR_INVALID_ARG;
     if (K % 8 || ldx % 8) return QOQ_ERR_SHAPE;
     if (M == 0) return QOQ_OK;
     if (!X || !gamma || !qx || !sx || !aligned16(X) || !aligned16(gamma) || (reinterpret_cast<uintptr_t>(qx) & 7u))

@@ -74,6 +74,21 @@ def test_rmsnorm_quantize_prefill_size(gpu_lib):
     assert_same(got, oracle.rmsnorm_quantize(X, g, 1e-5), "rmsnorm M=4096")
 
 
+@pytest.mark.parametrize("K", [256, 4096, 16392])
+def test_rmsnorm_exact_fp16_ties(gpu_lib, K):
+    """Rows whose fp64 y lands EXACTLY on fp16 rounding midpoints (ties to even, Q24): x in {3, 1}
+    with mean(x²) = 4 (r = 1/2 exactly at eps = 0) and γ = 1 + 2^-10, so y = 1.5 (1 + 2^-10) is
+    1.5 ulp above 1.5 — the fp32 fast path must hand these to the exact path."""
+    X = np.tile(np.array([3, 3, 3, 1, 1, 1, 1, 1], np.float16), (4, K // 8))
+    X[1] *= -1
+    X[2] = np.roll(X[2], 3)
+    g = np.full(K, 1 + 2.0 ** -10, np.float16)
+    got = gpu_lib.rmsnorm_quantize(to_dev(X), to_dev(g), 0.0)
+    assert_same(got, oracle.rmsnorm_quantize(X, g, 0.0), f"rmsnorm ties K={K}")
+    Y = oracle.rmsnorm_fp16(X, g, 0.0)
+    assert Y[0, 0] == np.float16(1.5 + 2 * 2.0 ** -10)       # the tie rounded to even (up here)
+
+
 SILU_SHAPES = [(1, 8), (3, 200), (16, 256), (7, 1032), (64, 14336), (2, 16384), (3, 16392), (2, 28672)]
 
 
@@ -84,6 +99,10 @@ def test_silu_mul_quantize_bit_exact(gpu_lib, M, K):
         GU[1] = 0                                                                # all-zero row
     if M > 2:                                                                    # extremes: exp over/underflow
         GU[2, :8] = np.array([65504, -65504, 40, -40, 11.09, -11.09, 1e-7, -6e-8], np.float16)
+    if M > 3:                                                                    # exact fp16 ties: silu(48) = 48
+        GU[3, :K] = np.float16(48.0)                                             # in fp64, 48 (1 + 2^-10) is a
+        GU[3, K:] = np.float16(1 + 2.0 ** -10)                                   # midpoint (1.5 ulp above 48)
+        GU[3, 1:K:2] = np.float16(-3.0)
     got = gpu_lib.silu_mul_quantize(to_dev(GU))
     assert_same(got, oracle.silu_mul_quantize(GU), f"silu M={M} K={K}")
 
