@@ -268,6 +268,7 @@ def main():
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-fused-block", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-streams", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="per-projection GEMM breakdown and M sweep")
     ap.add_argument("--no-per-channel", action="store_true",
@@ -445,7 +446,8 @@ def main():
 
     # ---- e2e through the C ABI with host buffers (H2D + quantize + GEMM + D2H per GEMM)
     if not args.no_e2e:
-        line["e2e"] = e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes)
+        line["e2e"] = e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes,
+                                  nstreams=args.e2e_streams)
 
     if not args.no_prefill:
         line["prefill"] = prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream)
@@ -465,7 +467,7 @@ def main():
     return 0
 
 
-def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes, nstreams=2):
+def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes, nstreams=6):
     """End to end through the C ABI (qoq_linear_host: pinned host X -> device -> w4a8_linear ->
     pinned host Y) for every GEMM of the step. Consecutive calls alternate over `nstreams` CUDA
     streams (each with its own scratch and host buffers), so one call's D2H copy overlaps the next

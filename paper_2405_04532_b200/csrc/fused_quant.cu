@@ -14,6 +14,7 @@
 // dependent GEMM's CTAs stream their weights while the row kernel runs.
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "qoq_internal.h"
 #include "qoq_quant.cuh"
@@ -289,11 +290,15 @@ __global__ void __launch_bounds__(1024) silu_mul_quant_kernel(const __half* __re
 }
 
 namespace {
-// Few rows (decode): 512-1024 threads per row so each thread's chain of loads is short; many rows
+// Few rows (decode): 1024 threads per row (measured best at M = 64) so each thread's chain of loads is short; many rows
 // (prefill): K/32 threads (128..256) per row, many CTAs per SM overlapping their reduction latencies.
 int row_threads(int M, int K) {
+    if (const char* e = getenv("QOQ_FQ_THREADS")) {   // tuning override (tools only): 128..1024
+        const int t = atoi(e);
+        if (t >= 128 && t <= 1024 && t % 32 == 0) return t;
+    }
     if (M >= 2 * 148) return K >= 8192 ? 256 : 128;
-    return K >= 8192 ? 1024 : 512;
+    return 1024;
 }
 
 cudaLaunchConfig_t row_cfg(int M, int K, cudaStream_t st, cudaLaunchAttribute* attr, bool pdl) {

@@ -1,5 +1,6 @@
 """Summarise an ncu launch list (gpu__time_duration.sum) of bench.py: the decode step's kernels only
-(each per-token quantizer launch at grid (M,1,1) and the W4A8 GEMM launch that follows it).
+(each per-token quantizer launch at grid (M,1,1) — plain, or fused into RMSNorm / SiLU·mul in the
+fused_block step — and the W4A8 GEMM launch that follows it).
 
   python tools/launch_share.py gpurun_out/launches.csv [M]
 """
@@ -17,8 +18,9 @@ def main(path, M=64):
                 for r in rows[i + 1:] if len(r) > col["Metric Value"]]
     t = defaultdict(list)
     for a, b in zip(launches, launches[1:]):
-        if "quantize_act_kernel" in a[0] and a[1] == f"({M}, 1, 1)" and "w4a8_gemm_kernel" in b[0]:
-            t["quantize_act_kernel"].append(a[3])
+        q = next((n for n in ("quantize_act_kernel", "rmsnorm_quant_kernel", "silu_mul_quant_kernel") if n in a[0]), None)
+        if q and a[1] == f"({M}, 1, 1)" and "w4a8_gemm_kernel" in b[0]:
+            t[q].append(a[3])
             t[f"w4a8_gemm_kernel grid {b[1]} block {b[2]}"].append(b[3])
     tot = sum(sum(v) for v in t.values())
     print(f"decode-step launches (M={M}), ncu serialized cold-cache times:")
