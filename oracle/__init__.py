@@ -70,6 +70,11 @@ def lib() -> ctypes.CDLL:
                 "oracle_silu_f64": (ctypes.c_double, [ctypes.c_double]),
                 "oracle_silu_mul_fp16": (I, [P, P, I, I, I, P]),
                 "oracle_silu_mul_quantize": (I, [P, P, I, I, I, P, P, P]),
+                "oracle_kv4_quantize": (I, [P, I, I, P, P, P]),
+                "oracle_kv4_page_bytes": (ctypes.c_size_t, [I, I, I]),
+                "oracle_kv4_store": (I, [P, P, P, P, P, P, I, I, I, I, P, P]),
+                "oracle_kv4_dequant": (I, [P, P, P, I, I, P]),
+                "oracle_attention_f64": (I, [P, P, P, I, I, I, I, P]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -364,3 +369,55 @@ def silu_mul_quantize(G: np.ndarray, U: np.ndarray | None = None, K: int | None 
     _check(lib().oracle_silu_mul_quantize(_p(G), _p(U), M, K, K, _p(qx), _p(sx), _p(tx)),
            "silu_mul_quantize")
     return qx, sx.view(np.float16), tx
+
+
+# ---- NEXT-4: KV4 cache + decode attention (§5.3; Q27-Q29) ----
+
+def kv4_quantize(X: np.ndarray):
+    """Rows of D fp16 values -> (q u8 [rows][D], s fp16 [rows], z fp16 [rows]) (Q27)."""
+    X = _u16(X)
+    rows, D = X.shape
+    q = np.empty((rows, D), np.uint8)
+    s = np.empty(rows, np.uint16)
+    z = np.empty(rows, np.uint16)
+    _check(lib().oracle_kv4_quantize(_p(X), rows, D, _p(q), _p(s), _p(z)), "kv4_quantize")
+    return q, s.view(np.float16), z.view(np.float16)
+
+
+def kv4_page_bytes(H_kv: int, D: int, P: int) -> int:
+    return lib().oracle_kv4_page_bytes(H_kv, D, P)
+
+
+def kv4_store(k, v, block_table: np.ndarray, n_pages: int, P: int, pages: np.ndarray | None = None):
+    """k, v: (q [T][H_kv][D], s [T][H_kv], z [T][H_kv]) -> pages u8 [n_pages * page_bytes] (Q28)."""
+    qk, sk, zk = k
+    qv, sv, zv = v
+    T, H_kv, D = qk.shape
+    if pages is None:
+        pages = np.zeros(n_pages * kv4_page_bytes(H_kv, D, P), np.uint8)
+    bt = np.ascontiguousarray(block_table, np.int32)
+    _check(lib().oracle_kv4_store(_p(np.ascontiguousarray(qk)), _p(_u16(sk)), _p(_u16(zk)),
+                                  _p(np.ascontiguousarray(qv)), _p(_u16(sv)), _p(_u16(zv)),
+                                  T, H_kv, D, P, _p(bt), _p(pages)), "kv4_store")
+    return pages
+
+
+def kv4_dequant(q: np.ndarray, s: np.ndarray, z: np.ndarray) -> np.ndarray:
+    shp = q.shape
+    q2 = np.ascontiguousarray(q.reshape(-1, shp[-1]))
+    out = np.empty(q2.shape, np.float64)
+    _check(lib().oracle_kv4_dequant(_p(q2), _p(_u16(s.reshape(-1))), _p(_u16(z.reshape(-1))), q2.shape[0],
+                                    q2.shape[1], _p(out)), "kv4_dequant")
+    return out.reshape(shp)
+
+
+def attention_f64(Q: np.ndarray, Khat: np.ndarray, Vhat: np.ndarray) -> np.ndarray:
+    """Q [H][D] fp16, Khat/Vhat [T][H_kv][D] fp64 -> O [H][D] fp64 (Q29)."""
+    Q = _u16(Q)
+    H, D = Q.shape
+    T, H_kv, _ = Khat.shape
+    O = np.empty((H, D), np.float64)
+    _check(lib().oracle_attention_f64(_p(Q), _p(np.ascontiguousarray(Khat, np.float64)),
+                                      _p(np.ascontiguousarray(Vhat, np.float64)), T, H, H_kv, D, _p(O)),
+           "attention_f64")
+    return O

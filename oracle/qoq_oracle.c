@@ -447,3 +447,89 @@ int oracle_silu_mul_quantize(const uint16_t* G, const uint16_t* U, int M, int K,
     free(H);
     return rc;
 }
+
+/* ---------------- NEXT-4: KV4 cache and decode attention (§5.3) ----------------
+ * Q27: each (token, kv head) vector of D values is quantized with the per-channel rule of Q20-Q22 (Eq. 2,
+ * asymmetric UINT4, FP16 scale; the integer zero point stored as FP16, "FP16 scaling factors and
+ * zero points for each head"). Q28: page layout. Q29: attention o_h = softmax(q_h K^T/√D) V
+ * on the dequantized cache, kv head = h / (H / H_kv) (GQA). */
+
+int oracle_kv4_quantize(const uint16_t* X, int rows, int D, uint8_t* q, uint16_t* s, uint16_t* z) {
+    uint8_t* zz = (uint8_t*)malloc((size_t)(rows > 0 ? rows : 1));
+    if (!zz) return -3;
+    int rc = oracle_pc_quantize(X, rows, D, q, s, zz);
+    for (int i = 0; rc == 0 && i < rows; ++i) z[i] = oracle_f2h_rn((float)zz[i]);
+    free(zz);
+    return rc;
+}
+
+size_t oracle_kv4_page_bytes(int H_kv, int D, int P) { return (size_t)H_kv * P * (D + 8); }
+
+/* Store T tokens of one sequence (codes q*[T][H_kv][D], params s*, z* [T][H_kv]) into pages following
+ * block_table (token t -> page block_table[t / P], slot t % P). Page layout per kv head h, at
+ * page + h * P * (D + 8): K codes [P][D/2] (byte j = q[2j] | q[2j+1] << 4), V codes [P][D/2],
+ * K params [P][s, z] fp16, V params [P][s, z] fp16. */
+int oracle_kv4_store(const uint8_t* qk, const uint16_t* sk, const uint16_t* zk, const uint8_t* qv,
+                     const uint16_t* sv, const uint16_t* zv, int T, int H_kv, int D, int P,
+                     const int32_t* block_table, uint8_t* pages) {
+    if (D % 2 || P <= 0 || T < 0) return -1;
+    size_t pb = oracle_kv4_page_bytes(H_kv, D, P), hb = (size_t)P * (D + 8);
+    for (int t = 0; t < T; ++t)
+        for (int h = 0; h < H_kv; ++h) {
+            uint8_t* base = pages + (size_t)block_table[t / P] * pb + (size_t)h * hb;
+            int o = t % P;
+            size_t row = ((size_t)t * H_kv + h) * D;
+            for (int j = 0; j < D / 2; ++j) {
+                base[(size_t)o * (D / 2) + j] = (uint8_t)(qk[row + 2 * j] | (qk[row + 2 * j + 1] << 4));
+                base[(size_t)P * (D / 2) + (size_t)o * (D / 2) + j] = (uint8_t)(qv[row + 2 * j] | (qv[row + 2 * j + 1] << 4));
+            }
+            uint16_t* par = (uint16_t*)(base + (size_t)P * D);
+            par[2 * o] = sk[(size_t)t * H_kv + h];
+            par[2 * o + 1] = zk[(size_t)t * H_kv + h];
+            par[2 * P + 2 * o] = sv[(size_t)t * H_kv + h];
+            par[2 * P + 2 * o + 1] = zv[(size_t)t * H_kv + h];
+        }
+    return 0;
+}
+
+/* Dequantize: xhat = (q - z) * s in fp64 (exact: an 11-bit scale times an integer in [-15, 15]). */
+int oracle_kv4_dequant(const uint8_t* q, const uint16_t* s, const uint16_t* z, int rows, int D, double* xhat) {
+    for (int i = 0; i < rows; ++i)
+        for (int d = 0; d < D; ++d)
+            xhat[(size_t)i * D + d] = ((double)q[(size_t)i * D + d] - (double)oracle_h2f(z[i])) * (double)oracle_h2f(s[i]);
+    return 0;
+}
+
+/* Decode attention for one sequence, the definition (§2.1; P:412 GQA via kv head h / (H / H_kv)):
+ * o[h] = Σ_t p_t v_t, p = softmax_t(q_h · k_t / sqrt(D)), all in fp64 (max-subtracted exp).
+ * Q [H][D] fp16; Khat, Vhat [T][H_kv][D] fp64; O [H][D] fp64. */
+int oracle_attention_f64(const uint16_t* Q, const double* Khat, const double* Vhat, int T, int H, int H_kv, int D,
+                         double* O) {
+    if (T <= 0 || H_kv <= 0 || H % H_kv) return -1;
+    double* sc = (double*)malloc((size_t)T * sizeof(double));
+    if (!sc) return -3;
+    int r = H / H_kv;
+    for (int h = 0; h < H; ++h) {
+        int g = h / r;
+        double mx = -INFINITY;
+        for (int t = 0; t < T; ++t) {
+            double a = 0.0;
+            for (int d = 0; d < D; ++d)
+                a += (double)oracle_h2f(Q[(size_t)h * D + d]) * Khat[((size_t)t * H_kv + g) * D + d];
+            sc[t] = a / sqrt((double)D);
+            if (sc[t] > mx) mx = sc[t];
+        }
+        double L = 0.0;
+        for (int t = 0; t < T; ++t) {
+            sc[t] = exp(sc[t] - mx);
+            L += sc[t];
+        }
+        for (int d = 0; d < D; ++d) {
+            double acc = 0.0;
+            for (int t = 0; t < T; ++t) acc += sc[t] * Vhat[((size_t)t * H_kv + g) * D + d];
+            O[(size_t)h * D + d] = acc / L;
+        }
+    }
+    free(sc);
+    return 0;
+}

@@ -128,6 +128,23 @@ int oracle_silu_mul_fp16(const uint16_t* G, const uint16_t* U, int M, int K, int
 int oracle_silu_mul_quantize(const uint16_t* G, const uint16_t* U, int M, int K, int ldg,
                              int8_t* qx, uint16_t* sx, int32_t* tx);
 
+/* ---------------- NEXT-4: KV4 cache + decode attention (§5.3) ----------------
+ * Readings Q27-Q29. */
+/* per-(token, kv head) asymmetric UINT4 of rows of D values: the Q20-Q22 rule (oracle_pc_quantize),
+ * zero point returned as fp16 bits. q [rows][D]; s, z [rows]. */
+int oracle_kv4_quantize(const uint16_t* X, int rows, int D, uint8_t* q, uint16_t* s, uint16_t* z);
+/* bytes of one page (P tokens, all kv heads, K and V): H_kv * P * (D + 8) */
+size_t oracle_kv4_page_bytes(int H_kv, int D, int P);
+/* write T tokens of one sequence into pages (layout in qoq_oracle.c / DESIGN.md §4) */
+int oracle_kv4_store(const uint8_t* qk, const uint16_t* sk, const uint16_t* zk, const uint8_t* qv,
+                     const uint16_t* sv, const uint16_t* zv, int T, int H_kv, int D, int P,
+                     const int32_t* block_table, uint8_t* pages);
+/* xhat = (q - z) s in fp64 */
+int oracle_kv4_dequant(const uint8_t* q, const uint16_t* s, const uint16_t* z, int rows, int D, double* xhat);
+/* o_h = softmax(q_h K^T / sqrt(D)) V over T tokens, kv head h / (H / H_kv); fp64 */
+int oracle_attention_f64(const uint16_t* Q, const double* Khat, const double* Vhat, int T, int H, int H_kv, int D,
+                         double* O);
+
 /* Number of OpenMP threads the oracle's parallel loops use (1 without OpenMP). */
 int oracle_num_threads(void);
 
