@@ -40,7 +40,7 @@ typedef enum {
 const char* qoq_status_string(int status);
 /* ABI version of this header (incremented on any signature or layout change). */
 int qoq_abi_version(void);
-#define QOQ_ABI_VERSION 4
+#define QOQ_ABI_VERSION 5
 
 /* ----------------------------------------------------------------------------------------------
  * Packed weight layout (frozen). The B200 form of "store the weights in the order
@@ -182,8 +182,33 @@ int qoq_rmsnorm_quantize(const void* X_fp16, int ldx, const void* gamma_fp16, do
 int qoq_silu_mul_quantize(const void* gate_fp16, const void* up_fp16, int ldg, int M, int K,
                           int8_t* qx, void* sx_fp16, int32_t* tx, void* stream);
 
+/* ---- KV4 cache and decode attention (NEXT-4; §5.3; Q27-Q29) ----
+ * "per-head asymmetric INT4 quantization on KV cache", "FP16 scaling factors and zero points for
+ * each head immediately following the quantized KV features in each KV cache page".
+ * Page (one layer, page_size P tokens, all H_kv heads; D must be 128): per kv head g, at byte g*P*(D+8):
+ *   K codes [P][D/2] (byte j = q[2j] | q[2j+1] << 4), V codes [P][D/2], K (s, z) fp16 pairs [P],
+ *   V (s, z) fp16 pairs [P]. Token t of a sequence lives in page block_table[t / P], slot t % P.
+ * Quantization of each (token, head) row: the per-channel rule of qoq_pc_quantize_weights
+ *   (s = fp16(fp32(max - min) / 15), z = clamp(⌈-min/s⌋, 0, 15) stored as fp16, q = clamp(⌈x/s + z⌋, 0, 15)).
+ * qoq_kv4_page_bytes: H_kv * P * (D + 8); 0 if unsupported.
+ * qoq_kv4_append: K_fp16, V_fp16 [B][H_kv][D] (one new token per sequence); slots [B] int32 (device) =
+ *   page * P + offset of each sequence's new token; pages: the page pool (device, 16-byte aligned).
+ * qoq_kv4_decode_attention: O[b][h] = softmax(Q[b][h] · K̂ᵀ / sqrt(D)) · V̂ over the first seq_lens[b] tokens
+ *   of sequence b, kv head h / (H / H_kv) (H / H_kv in {1, 2, 4, 8}); fp32 arithmetic, fp16 output.
+ *   Q_fp16, O_fp16 [B][H][D]; block_table [B][max_pages] int32; seq_lens [B] int32 (device; a length
+ *   <= 0 gives zeros; lengths must not exceed max_pages * P).
+ * Errors: D != 128 or an unsupported H / H_kv -> QOQ_ERR_UNSUPPORTED; H % H_kv -> QOQ_ERR_SHAPE;
+ * null / misaligned pointers, non-positive sizes -> QOQ_ERR_INVALID_ARG. B == 0 is a no-op. */
+size_t qoq_kv4_page_bytes(int H_kv, int D, int page_size);
+int qoq_kv4_append(const void* K_fp16, const void* V_fp16, const int32_t* slots, int B, int H_kv, int D,
+                   int page_size, void* pages, void* stream);
+int qoq_kv4_decode_attention(const void* Q_fp16, const void* pages, const int32_t* block_table,
+                             const int32_t* seq_lens, int B, int H, int H_kv, int D, int page_size, int max_pages,
+                             void* O_fp16, void* stream);
+
 /* Kernels launched per successful call (launch accounting for benchmarks):
- * quantize_weights 2, quantize_activations_per_token 1, rmsnorm_quantize 1, silu_mul_quantize 1, w4a8_gemm 1, w4a8_gemm_i32 1,
+ * quantize_weights 2, quantize_activations_per_token 1, rmsnorm_quantize 1, silu_mul_quantize 1,
+ * kv4_append 1, kv4_decode_attention 1, w4a8_gemm 1, w4a8_gemm_i32 1,
  * pc_quantize_weights 2, pc_w4a8_gemm 1, pc_w4a8_gemm_i32 1,
  * w4a8_linear 2 (1 when fused: QOQ_LINEAR_FUSED=1 and M <= 64), linear_host as w4a8_linear
  * (plus 2 async copies). */

@@ -23,11 +23,11 @@ LIB_PATH = os.path.join(_HERE, "libqoq_b200.so" if not os.environ.get("QOQ_LIB_V
                         else f"libqoq_b200_{os.environ['QOQ_LIB_VARIANT']}.so")
 GROUP = 128
 TILE_BYTES = 8448
-ABI_VERSION = 4
+ABI_VERSION = 5
 # kernels launched per call (matches include/qoq_b200.h)
 LAUNCHES = {"quantize_weights": 2, "quantize_activations_per_token": 1, "w4a8_gemm": 1,
             "w4a8_gemm_i32": 1, "pc_quantize_weights": 2, "pc_w4a8_gemm": 1, "pc_w4a8_gemm_i32": 1,
-            "rmsnorm_quantize": 1, "silu_mul_quantize": 1}
+            "rmsnorm_quantize": 1, "silu_mul_quantize": 1, "kv4_append": 1, "kv4_decode_attention": 1}
 FUSE_MAX_M = 64   # w4a8_linear / linear_host with QOQ_LINEAR_FUSED=1: one fused kernel up to this M
 
 
@@ -79,6 +79,9 @@ def load() -> ctypes.CDLL:
             "qoq_pc_w4a8_gemm_i32": (I, [P, P, P, P, I, I, I, P, I, P, Z, P]),
             "qoq_rmsnorm_quantize": (I, [P, I, P, ctypes.c_double, I, I, P, P, P, P]),
             "qoq_silu_mul_quantize": (I, [P, P, I, I, I, P, P, P, P]),
+            "qoq_kv4_page_bytes": (Z, [I, I, I]),
+            "qoq_kv4_append": (I, [P, P, P, I, I, I, I, P, P]),
+            "qoq_kv4_decode_attention": (I, [P, P, P, P, I, I, I, I, I, I, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -214,6 +217,31 @@ def silu_mul_quantize(gate_up: torch.Tensor, K: int | None = None, want_tx: bool
            load().qoq_silu_mul_quantize(ctypes.c_void_p(base), ctypes.c_void_p(base + 2 * K), ld, M, K,
                                         _ptr(qx), _ptr(sx), _ptr(tx), _stream(stream)))
     return qx, sx, tx
+
+
+def kv4_page_bytes(H_kv: int, D: int = 128, page_size: int = 64) -> int:
+    return load().qoq_kv4_page_bytes(H_kv, D, page_size)
+
+
+def kv4_append(K: torch.Tensor, V: torch.Tensor, slots: torch.Tensor, pages: torch.Tensor, page_size: int = 64,
+               stream=None):
+    """Quantize one new token per sequence into the KV4 page pool (NEXT-4; C-ABI qoq_kv4_append).
+    K, V [B][H_kv][D] fp16; slots [B] int32 (page * page_size + offset); pages uint8 pool."""
+    B, H_kv, D = K.shape
+    _check("qoq_kv4_append", load().qoq_kv4_append(_ptr(K), _ptr(V), _ptr(slots), B, H_kv, D, page_size,
+                                                   _ptr(pages), _stream(stream)))
+
+
+def kv4_decode_attention(Q: torch.Tensor, pages: torch.Tensor, block_table: torch.Tensor, seq_lens: torch.Tensor,
+                         H_kv: int, page_size: int = 64, out=None, stream=None):
+    """Decode attention over the KV4 cache (§5.3; C-ABI qoq_kv4_decode_attention): Q [B][H][D] fp16 ->
+    O [B][H][D] fp16."""
+    B, H, D = Q.shape
+    O = torch.empty_like(Q) if out is None else out
+    _check("qoq_kv4_decode_attention",
+           load().qoq_kv4_decode_attention(_ptr(Q), _ptr(pages), _ptr(block_table), _ptr(seq_lens), B, H, H_kv,
+                                           D, page_size, block_table.shape[1], _ptr(O), _stream(stream)))
+    return O
 
 
 class Workspace:

@@ -197,6 +197,47 @@ int qoq_silu_mul_quantize(const void* gate, const void* up, int ldg, int M, int 
                    cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
 }
 
+size_t qoq_kv4_page_bytes(int H_kv, int D, int page_size) {
+    if (H_kv <= 0 || D != 128 || page_size <= 0) return 0;
+    return (size_t)H_kv * page_size * (D + 8);
+}
+
+namespace {
+int kv4_shape_status(int B, int H, int H_kv, int D, int P) {
+    if (B < 0 || H <= 0 || H_kv <= 0 || P <= 0) return QOQ_ERR_INVALID_ARG;
+    if (D != 128) return QOQ_ERR_UNSUPPORTED;
+    if (H % H_kv) return QOQ_ERR_SHAPE;
+    const int r = H / H_kv;
+    if (r != 1 && r != 2 && r != 4 && r != 8) return QOQ_ERR_UNSUPPORTED;
+    return QOQ_OK;
+}
+}  // namespace
+
+int qoq_kv4_append(const void* K, const void* V, const int32_t* slots, int B, int H_kv, int D, int page_size,
+                   void* pages, void* stream) {
+    int rc = kv4_shape_status(B, H_kv, H_kv, D, page_size);
+    if (rc) return rc;
+    if (B == 0) return QOQ_OK;
+    if (!K || !V || !slots || !pages || !aligned16(K) || !aligned16(V) || !aligned16(pages)) return QOQ_ERR_INVALID_ARG;
+    if ((rc = check_arch(nullptr))) return rc;
+    return launch_kv4_append(K, V, slots, B, H_kv, page_size, static_cast<uint8_t*>(pages),
+                             static_cast<cudaStream_t>(stream)) == cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
+int qoq_kv4_decode_attention(const void* Q, const void* pages, const int32_t* block_table, const int32_t* seq_lens,
+                             int B, int H, int H_kv, int D, int page_size, int max_pages, void* O, void* stream) {
+    int rc = kv4_shape_status(B, H, H_kv, D, page_size);
+    if (rc) return rc;
+    if (max_pages <= 0) return QOQ_ERR_INVALID_ARG;
+    if (B == 0) return QOQ_OK;
+    if (!Q || !pages || !block_table || !seq_lens || !O || !aligned16(Q) || !aligned16(O) || !aligned16(pages))
+        return QOQ_ERR_INVALID_ARG;
+    if ((rc = check_arch(nullptr))) return rc;
+    return launch_kv4_decode_attention(Q, static_cast<const uint8_t*>(pages), block_table, seq_lens, B, H, H_kv,
+                                       page_size, max_pages, O, static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
 size_t qoq_gemm_workspace_bytes(int M, int N, int K) {
     if (gemm_shape_status(M, N, K, 128) != QOQ_OK || M == 0) return 0;
     return plan_gemm(M, N, K, num_sms_or_default()).ws_bytes;

@@ -67,4 +67,11 @@ cudaError_t launch_rmsnorm_quantize(const void* X, int ldx, const void* gamma, d
 cudaError_t launch_silu_mul_quantize(const void* G, const void* U, int ldg, int M, int K, int8_t* qx, void* sx,
                                      int32_t* tx, cudaStream_t st, bool pdl);
 
+// NEXT-4: KV4 cache + decode attention (kv4_attention.cu), D = 128
+cudaError_t launch_kv4_append(const void* K, const void* V, const int32_t* slots, int B, int H_kv, int P,
+                              uint8_t* pages, cudaStream_t st);
+cudaError_t launch_kv4_decode_attention(const void* Q, const uint8_t* pages, const int32_t* block_table,
+                                        const int32_t* seq_lens, int B, int H, int H_kv, int P, int max_pages,
+                                        void* O, cudaStream_t st);
+
 }  // namespace qoq

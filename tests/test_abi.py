@@ -45,7 +45,7 @@ def test_library_is_sm100a_only(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert lib.qoq_abi_version() == 4
+    assert lib.qoq_abi_version() == 5
     for s in range(0, 8):
         assert lib.qoq_status_string(s)
 
@@ -129,3 +129,20 @@ def test_fused_quantizer_validation(lib):
     assert lib.qoq_silu_mul_quantize(fake, P((1 << 20) + 2), 512, 4, 256, fake, fake, None, None) == 1
     assert lib.qoq_silu_mul_quantize(fake, None, 512, 4, 256, fake, fake, None, None) == 1
     assert lib.qoq_silu_mul_quantize(fake, fake, 512, 0, 256, fake, fake, None, None) == 0
+
+
+def test_kv4_validation(lib):
+    """NEXT-4 entries: page size query, D / GQA-ratio / shape errors and the B == 0 no-op, host-side."""
+    P = ctypes.c_void_p
+    fake = P(1 << 20)
+    assert lib.qoq_kv4_page_bytes(8, 128, 64) == 8 * 64 * 136
+    assert lib.qoq_kv4_page_bytes(8, 64, 64) == 0
+    assert lib.qoq_kv4_append(fake, fake, fake, 4, 8, 64, 64, fake, None) == 3            # D != 128
+    assert lib.qoq_kv4_append(fake, fake, None, 4, 8, 128, 64, fake, None) == 1           # slots missing
+    assert lib.qoq_kv4_append(fake, fake, fake, 0, 8, 128, 64, fake, None) == 0
+    args = (fake, fake, fake, fake, 4, 32, 8, 128, 64, 16, fake, None)
+    assert lib.qoq_kv4_decode_attention(fake, fake, fake, fake, 4, 30, 8, 128, 64, 16, fake, None) == 2
+    assert lib.qoq_kv4_decode_attention(fake, fake, fake, fake, 4, 48, 3, 128, 64, 16, fake, None) == 3
+    assert lib.qoq_kv4_decode_attention(fake, fake, fake, fake, 4, 32, 8, 128, 64, 0, fake, None) == 1
+    assert lib.qoq_kv4_decode_attention(P((1 << 20) + 8), *args[1:]) == 1
+    assert lib.qoq_kv4_decode_attention(fake, fake, fake, fake, 0, 32, 8, 128, 64, 16, fake, None) == 0
