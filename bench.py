@@ -267,6 +267,7 @@ def main():
     ap.add_argument("--prefill-M", type=int, default=4096)
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-fused-block", action="store_true")
+    ap.add_argument("--no-kv4", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-streams", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -443,6 +444,10 @@ def main():
     if not args.no_fused_block and world == 1:
         line["fused_block"] = fused_block_measure(qoq, torch, args, shapes, packed, layers, dev, stream, X,
                                                   quant_out, Ybuf, ws, timed)
+
+    # ---- KV4 decode attention (NEXT-4, §5.3): the paper's other hot kernel, Llama-3-8B heads
+    if not args.no_kv4 and world == 1:
+        line["kv4_attention"] = kv4_measure(qoq, torch, dev, stream, timed)
 
     # ---- e2e through the C ABI with host buffers (H2D + quantize + GEMM + D2H per GEMM)
     if not args.no_e2e:
@@ -672,6 +677,49 @@ def fused_block_measure(qoq, torch, args, shapes, packed, layers, dev, stream, X
             del ins, o
     out["kernels"] = kern
     return out
+
+
+def kv4_measure(qoq, torch, dev, stream, timed, B=64, T=1024, H=32, H_kv=8, D=128, P=64, layers=4):
+    """Decode attention over a paged KV4 cache (qoq_kv4_decode_attention): B sequences x T tokens,
+    Llama-3-8B heads, one call per layer over `layers` distinct caches (> L2 in total). Algorithmic bytes
+    per call: the cache (K + V codes D bytes + 8 bytes of fp16 scale/zero per token and kv head), Q, O and
+    the block table. The cache is filled on the device with qoq_kv4_append from seeded normals."""
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(31)
+    npg = T // P
+    pb = qoq.kv4_page_bytes(H_kv, D, P)
+    caches = []
+    with torch.cuda.stream(stream):
+        for l in range(layers):
+            pages = torch.zeros(B * npg * pb, dtype=torch.uint8, device=dev)
+            bt = torch.randperm(B * npg, generator=gen, device=dev).to(torch.int32).view(B, npg)
+            for t in range(T):
+                Kt = torch.randn(B, H_kv, D, generator=gen, device=dev).half()
+                Vt = torch.randn(B, H_kv, D, generator=gen, device=dev).half()
+                slots = (bt[:, t // P] * P + t % P).contiguous()
+                qoq.kv4_append(Kt, Vt, slots, pages, P, stream=stream)
+            caches.append((pages, bt))
+        lens = torch.full((B,), T, dtype=torch.int32, device=dev)
+        Q = torch.randn(B, H, D, generator=gen, device=dev).half()
+        O = torch.empty_like(Q)
+        stream.synchronize()
+
+        def run():
+            for pages, bt in caches:
+                qoq.kv4_decode_attention(Q, pages, bt, lens, H_kv, P, out=O, stream=stream)
+
+        run()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            run()
+        reps = 10
+        us = timed(g, reps, 3) / reps / layers * 1e3
+    nbytes = B * T * H_kv * (D + 8) + 2 * 2 * B * H * D + 4 * B * npg + 4 * B
+    peak, _ = load_peaks()
+    gbps = nbytes / (us * 1e-6) / 1e9
+    return {"us": us, "GBps": gbps, "frac_hbm": gbps / peak, "algorithmic_bytes": nbytes,
+            "config": {"B": B, "seq_len": T, "H": H, "H_kv": H_kv, "D": D, "page_size": P, "layers_rotated": layers},
+            "paper_context": "A100 QServe KV4 kernel 0.28 ms at seq 1024 (Table P:507-526; other GPU/model: context only)"}
 
 
 def prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream):

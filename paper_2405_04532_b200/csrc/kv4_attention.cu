@@ -5,10 +5,12 @@
 //                            point — the per-channel rule of Q20-Q22 — and written into the sequence's
 //                            page slot ("dynamic", "updated on-the-fly").
 //   kv4_decode_attn_kernel : o_h = softmax(q_h K̂ᵀ/√D) V̂ for every query head h sharing kv head g (GQA),
-//                            one CTA per (sequence, kv head), 8 warps striding over the tokens with an
-//                            online softmax in fp32, merged across warps in shared memory.
+//                            a cluster of 4 CTAs per (sequence, kv head), 8 warps each striding over chunks
+//                            of 32/R tokens (butterfly-reduced scores, online softmax in fp32), the 32 warp
+//                            states merged by CTA 0 through distributed shared memory.
 // Dequantization (q − z)·s is exact in fp32 (an 11-bit scale times an integer in [−15, 15]); the paper's
 // FP16 arithmetic was an A100 CUDA-core roofline measure that B200 does not need.
+#include <cooperative_groups.h>
 #include <cuda_fp16.h>
 #include <cstdint>
 
@@ -19,6 +21,10 @@ namespace qoq {
 
 constexpr int kKvD = 128;       // head dim (Llama / Qwen families)
 constexpr int kAttnWarps = 8;
+#ifndef QOQ_KV4_SPLIT
+#define QOQ_KV4_SPLIT 2
+#endif
+constexpr int kAttnSplit = QOQ_KV4_SPLIT;   // CTAs (one thread-block cluster) per (sequence, kv head), merged over DSMEM
 
 __device__ __forceinline__ size_t kv_head_bytes(int P) { return (size_t)P * (kKvD + 8); }
 
@@ -74,14 +80,23 @@ __device__ __forceinline__ void dequant4(uint32_t c, float s, float zs, float (&
     for (int i = 0; i < 4; ++i) v[i] = __fmaf_rn((float)((c >> (4 * i)) & 15u), s, zs);   // q s - z s: exact
 }
 
+// Each warp walks its sequence in chunks of C = 32 / R tokens. For one chunk a lane (owning dims
+// 4l..4l+3) forms the 32 partial dot products (token c, head j) from its 4 dequantized K values; one
+// butterfly reduce-scatter (31 shuffles) leaves lane L with the full score of (c, j) = (L / R, L % R).
+// The chunk's softmax update runs on those lanes (max over the lanes of one head, one exp2 each), the
+// 32 probabilities are broadcast back by shuffles and the lane accumulates p · v̂ for its 4 dims.
 template <int R>
-__global__ void __launch_bounds__(kAttnWarps * 32) kv4_decode_attn_kernel(
+__global__ void __launch_bounds__(kAttnWarps * 32, 2) kv4_decode_attn_kernel(
     const __half* __restrict__ Q, const uint8_t* __restrict__ pages, const int32_t* __restrict__ block_table,
     const int32_t* __restrict__ seq_lens, int H_kv, int P, int max_pages, __half* __restrict__ O) {
+    constexpr int C = 32 / R;
     __shared__ float sm_m[kAttnWarps][R], sm_l[kAttnWarps][R];
     __shared__ float sm_acc[kAttnWarps][R][kKvD];
     pdl_wait();
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
     const int b = blockIdx.x, g = blockIdx.y, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int rank = (int)cluster.block_rank();           // = blockIdx.z: this CTA's share of the tokens
     const int H = H_kv * R;
     const int T = seq_lens[b];
     const float qscale = 1.4426950408889634f / sqrtf((float)kKvD);   // log2(e) / sqrt(D): scores in base 2
@@ -103,27 +118,75 @@ __global__ void __launch_bounds__(kAttnWarps * 32) kv4_decode_attn_kernel(
     }
     const size_t hb = kv_head_bytes(P), pb = (size_t)H_kv * hb;
     const int32_t* bt = block_table + (size_t)b * max_pages;
-    for (int t = w; t < T; t += kAttnWarps) {
-        const uint8_t* base = pages + (size_t)__ldg(bt + t / P) * pb + (size_t)g * hb;
-        const int o = t % P;
-        const uint32_t kc = __ldg(reinterpret_cast<const uint16_t*>(base + (size_t)o * (kKvD / 2)) + l);
-        const uint32_t vc = __ldg(reinterpret_cast<const uint16_t*>(base + (size_t)(P + o) * (kKvD / 2)) + l);
-        const __half2* par = reinterpret_cast<const __half2*>(base + (size_t)P * kKvD);
-        const float2 kp = __half22float2(par[o]), vp = __half22float2(par[P + o]);
-        float kh[4], vh[4];
-        dequant4(kc, kp.x, -kp.y * kp.x, kh);   // z s exact in fp32 (integer z <= 15 times an fp16 scale)
-        dequant4(vc, vp.x, -vp.y * vp.x, vh);
+    const int myc = l / R, myj = l % R;
+    for (int t0 = (rank * kAttnWarps + w) * C; t0 < T; t0 += kAttnSplit * kAttnWarps * C) {
+        uint32_t kc[C], vc[C], kp[C], vp[C];   // codes (16 bits), (s, z) fp16 pairs
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int t = t0 + c;
+            if (t < T) {
+                const uint8_t* base = pages + (size_t)__ldg(bt + t / P) * pb + (size_t)g * hb;
+                const int o = t % P;
+                kc[c] = __ldg(reinterpret_cast<const uint16_t*>(base + (size_t)o * (kKvD / 2)) + l);
+                vc[c] = __ldg(reinterpret_cast<const uint16_t*>(base + (size_t)(P + o) * (kKvD / 2)) + l);
+                const uint32_t* par = reinterpret_cast<const uint32_t*>(base + (size_t)P * kKvD);
+                kp[c] = __ldg(par + o);
+                vp[c] = __ldg(par + P + o);
+            } else {
+                kc[c] = vc[c] = kp[c] = vp[c] = 0u;
+            }
+        }
+        float v[32];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            float kh[4];
+            const float2 k2 = __half22float2(*reinterpret_cast<const __half2*>(&kp[c]));
+            dequant4(kc[c], k2.x, -k2.y * k2.x, kh);
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+                v[c * R + j] = qf[j][0] * kh[0] + qf[j][1] * kh[1] + qf[j][2] * kh[2] + qf[j][3] * kh[3];
+        }
+        // butterfly reduce-scatter: lane L ends with the warp sum of v[L]
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1) {
+            const bool up = (l & st) != 0;
+#pragma unroll
+            for (int i = 0; i < st; ++i) {
+                const float send = up ? v[i] : v[i + st];
+                const float keep = up ? v[i + st] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+            }
+        }
+        const float sc = (t0 + myc < T) ? v[0] : -INFINITY;
+        float cm = sc;                                          // chunk max over the lanes of head myj
+#pragma unroll
+        for (int x = R; x < 32; x <<= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, x));
+        float mj = m[0];
+#pragma unroll
+        for (int j = 1; j < R; ++j) mj = (myj == j) ? m[j] : mj;
+        const float mnew = fmaxf(mj, cm);
+        const float p = (sc == -INFINITY) ? 0.0f : exp2f(sc - mnew);
+        const float corr = (mj == -INFINITY) ? 0.0f : exp2f(mj - mnew);
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-            float sc = qf[j][0] * kh[0] + qf[j][1] * kh[1] + qf[j][2] * kh[2] + qf[j][3] * kh[3];
+            const float cj = __shfl_sync(0xffffffffu, corr, j);
+            m[j] = __shfl_sync(0xffffffffu, mnew, j);
+            lsum[j] *= cj;
 #pragma unroll
-            for (int x = 16; x > 0; x >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, x);
-            const float mn = fmaxf(m[j], sc);
-            const float corr = exp2f(m[j] - mn), p = exp2f(sc - mn);
-            m[j] = mn;
-            lsum[j] = lsum[j] * corr + p;
+            for (int i = 0; i < 4; ++i) acc[j][i] *= cj;
+        }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc[j][i] = acc[j][i] * corr + p * vh[i];
+        for (int c = 0; c < C; ++c) {
+            float vh[4];
+            const float2 v2 = __half22float2(*reinterpret_cast<const __half2*>(&vp[c]));
+            dequant4(vc[c], v2.x, -v2.y * v2.x, vh);
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const float pc = __shfl_sync(0xffffffffu, p, c * R + j);
+                lsum[j] += pc;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[j][i] = __fmaf_rn(pc, vh[i], acc[j][i]);
+            }
         }
     }
     // merge the 8 warps' partial softmax states
@@ -136,23 +199,41 @@ __global__ void __launch_bounds__(kAttnWarps * 32) kv4_decode_attn_kernel(
 #pragma unroll
         for (int i = 0; i < 4; ++i) sm_acc[w][j][4 * l + i] = acc[j][i];
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < R * kKvD; e += blockDim.x) {
-        const int j = e / kKvD, d = e % kKvD;
-        float M = -INFINITY;
+    cluster.sync();                                       // every CTA's warp states are in its smem
+    if (rank == 0) {
+        const float* rm[kAttnSplit];
+        const float* rl[kAttnSplit];
+        const float* ra[kAttnSplit];
 #pragma unroll
-        for (int x = 0; x < kAttnWarps; ++x) M = fmaxf(M, sm_m[x][j]);
-        float L = 0.0f, A = 0.0f;
-        if (M != -INFINITY) {
-#pragma unroll
-            for (int x = 0; x < kAttnWarps; ++x) {
-                const float f = exp2f(sm_m[x][j] - M);   // 0 for an idle warp (m = -inf)
-                L += sm_l[x][j] * f;
-                A += sm_acc[x][j][d] * f;
-            }
+        for (int r = 0; r < kAttnSplit; ++r) {
+            rm[r] = cluster.map_shared_rank(&sm_m[0][0], r);
+            rl[r] = cluster.map_shared_rank(&sm_l[0][0], r);
+            ra[r] = cluster.map_shared_rank(&sm_acc[0][0][0], r);
         }
-        O[((size_t)b * H + (size_t)g * R + j) * kKvD + d] = __float2half_rn(L > 0.0f ? A / L : 0.0f);
+        for (int e = threadIdx.x; e < R * kKvD; e += blockDim.x) {
+            const int j = e / kKvD, d = e % kKvD;
+            float M = -INFINITY;
+#pragma unroll
+            for (int r = 0; r < kAttnSplit; ++r)
+#pragma unroll
+                for (int x = 0; x < kAttnWarps; ++x) M = fmaxf(M, rm[r][x * R + j]);
+            float L = 0.0f, A = 0.0f;
+            if (M != -INFINITY) {
+#pragma unroll
+                for (int r = 0; r < kAttnSplit; ++r)
+#pragma unroll
+                    for (int x = 0; x < kAttnWarps; ++x) {
+                        const float mx = rm[r][x * R + j];
+                        if (mx == -INFINITY) continue;            // idle warp
+                        const float f = exp2f(mx - M);
+                        L += rl[r][x * R + j] * f;
+                        A += ra[r][(x * R + j) * kKvD + d] * f;
+                    }
+            }
+            O[((size_t)b * H + (size_t)g * R + j) * kKvD + d] = __float2half_rn(L > 0.0f ? A / L : 0.0f);
+        }
     }
+    cluster.sync();                                       // keep every CTA's smem alive until rank 0 is done
 }
 
 cudaError_t launch_kv4_append(const void* K, const void* V, const int32_t* slots, int B, int H_kv, int P,
@@ -165,17 +246,26 @@ cudaError_t launch_kv4_append(const void* K, const void* V, const int32_t* slots
 cudaError_t launch_kv4_decode_attention(const void* Q, const uint8_t* pages, const int32_t* block_table,
                                         const int32_t* seq_lens, int B, int H, int H_kv, int P, int max_pages,
                                         void* O, cudaStream_t st) {
-    const dim3 grid(B, H_kv), block(kAttnWarps * 32);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(B, H_kv, kAttnSplit);
+    cfg.blockDim = dim3(kAttnWarps * 32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = kAttnSplit;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     const __half* q = static_cast<const __half*>(Q);
     __half* o = static_cast<__half*>(O);
     switch (H / H_kv) {
-        case 1: kv4_decode_attn_kernel<1><<<grid, block, 0, st>>>(q, pages, block_table, seq_lens, H_kv, P, max_pages, o); break;
-        case 2: kv4_decode_attn_kernel<2><<<grid, block, 0, st>>>(q, pages, block_table, seq_lens, H_kv, P, max_pages, o); break;
-        case 4: kv4_decode_attn_kernel<4><<<grid, block, 0, st>>>(q, pages, block_table, seq_lens, H_kv, P, max_pages, o); break;
-        case 8: kv4_decode_attn_kernel<8><<<grid, block, 0, st>>>(q, pages, block_table, seq_lens, H_kv, P, max_pages, o); break;
+        case 1: return cudaLaunchKernelEx(&cfg, kv4_decode_attn_kernel<1>, q, pages, block_table, seq_lens, H_kv, P, max_pages, o);
+        case 2: return cudaLaunchKernelEx(&cfg, kv4_decode_attn_kernel<2>, q, pages, block_table, seq_lens, H_kv, P, max_pages, o);
+        case 4: return cudaLaunchKernelEx(&cfg, kv4_decode_attn_kernel<4>, q, pages, block_table, seq_lens, H_kv, P, max_pages, o);
+        case 8: return cudaLaunchKernelEx(&cfg, kv4_decode_attn_kernel<8>, q, pages, block_table, seq_lens, H_kv, P, max_pages, o);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 }  // namespace qoq
