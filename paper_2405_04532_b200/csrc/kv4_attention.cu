@@ -120,21 +120,30 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) kv4_decode_attn_kernel(
     const int32_t* bt = block_table + (size_t)b * max_pages;
     const int myc = l / R, myj = l % R;
     for (int t0 = (rank * kAttnWarps + w) * C; t0 < T; t0 += kAttnSplit * kAttnWarps * C) {
+        // a chunk never crosses a page (t0 % C == 0 and P % C == 0): one block-table lookup, the chunk's
+        // (s, z) pairs as 16-byte broadcast loads; tokens past T read as zeros (masked below)
         uint32_t kc[C], vc[C], kp[C], vp[C];   // codes (16 bits), (s, z) fp16 pairs
+        {
+            const uint8_t* base = pages + (size_t)__ldg(bt + t0 / P) * pb + (size_t)g * hb;
+            const int o0 = t0 % P;
+            const uint16_t* kcp = reinterpret_cast<const uint16_t*>(base + (size_t)o0 * (kKvD / 2)) + l;
+            const uint16_t* vcp = reinterpret_cast<const uint16_t*>(base + (size_t)(P + o0) * (kKvD / 2)) + l;
+            const uint4* kpp = reinterpret_cast<const uint4*>(base + (size_t)P * kKvD + (size_t)o0 * 4);
+            const uint4* vpp = reinterpret_cast<const uint4*>(base + (size_t)P * kKvD + (size_t)(P + o0) * 4);
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            const int t = t0 + c;
-            if (t < T) {
-                const uint8_t* base = pages + (size_t)__ldg(bt + t / P) * pb + (size_t)g * hb;
-                const int o = t % P;
-                kc[c] = __ldg(reinterpret_cast<const uint16_t*>(base + (size_t)o * (kKvD / 2)) + l);
-                vc[c] = __ldg(reinterpret_cast<const uint16_t*>(base + (size_t)(P + o) * (kKvD / 2)) + l);
-                const uint32_t* par = reinterpret_cast<const uint32_t*>(base + (size_t)P * kKvD);
-                kp[c] = __ldg(par + o);
-                vp[c] = __ldg(par + P + o);
-            } else {
-                kc[c] = vc[c] = kp[c] = vp[c] = 0u;
+            for (int c = 0; c < C; ++c) {
+                kc[c] = __ldg(kcp + c * (kKvD / 4));
+                vc[c] = __ldg(vcp + c * (kKvD / 4));
             }
+#pragma unroll
+            for (int c4 = 0; c4 < C / 4; ++c4) {
+                const uint4 a = __ldg(kpp + c4), bb = __ldg(vpp + c4);
+                kp[4 * c4] = a.x; kp[4 * c4 + 1] = a.y; kp[4 * c4 + 2] = a.z; kp[4 * c4 + 3] = a.w;
+                vp[4 * c4] = bb.x; vp[4 * c4 + 1] = bb.y; vp[4 * c4 + 2] = bb.z; vp[4 * c4 + 3] = bb.w;
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                if (t0 + c >= T) kc[c] = vc[c] = kp[c] = vp[c] = 0u;
         }
         float v[32];
 #pragma unroll
