@@ -190,14 +190,14 @@ int qoq_silu_mul_quantize(const void* gate_fp16, const void* up_fp16, int ldg, i
  *   V (s, z) fp16 pairs [P]. Token t of a sequence lives in page block_table[t / P], slot t % P.
  * Quantization of each (token, head) row: the per-channel rule of qoq_pc_quantize_weights
  *   (s = fp16(fp32(max - min) / 15), z = clamp(⌈-min/s⌋, 0, 15) stored as fp16, q = clamp(⌈x/s + z⌋, 0, 15)).
- * qoq_kv4_page_bytes: H_kv * P * (D + 8); 0 if unsupported. page_size must be a multiple of 32 (64 typical).
+ * qoq_kv4_page_bytes: H_kv * P * (D + 8); 0 if unsupported. page_size must be a multiple of 32, at most 256 (64 typical).
  * qoq_kv4_append: K_fp16, V_fp16 [B][H_kv][D] (one new token per sequence); slots [B] int32 (device) =
  *   page * P + offset of each sequence's new token; pages: the page pool (device, 16-byte aligned).
  * qoq_kv4_decode_attention: O[b][h] = softmax(Q[b][h] · K̂ᵀ / sqrt(D)) · V̂ over the first seq_lens[b] tokens
  *   of sequence b, kv head h / (H / H_kv) (H / H_kv in {1, 2, 4, 8}); fp32 arithmetic, fp16 output.
  *   Q_fp16, O_fp16 [B][H][D]; block_table [B][max_pages] int32; seq_lens [B] int32 (device; a length
  *   <= 0 gives zeros; lengths must not exceed max_pages * P).
- * Errors: D != 128, page_size % 32 != 0 or an unsupported H / H_kv -> QOQ_ERR_UNSUPPORTED; H % H_kv -> QOQ_ERR_SHAPE;
+ * Errors: D != 128, page_size % 32 != 0 or > 256, or an unsupported H / H_kv -> QOQ_ERR_UNSUPPORTED; H % H_kv -> QOQ_ERR_SHAPE;
  * null / misaligned pointers, non-positive sizes -> QOQ_ERR_INVALID_ARG. B == 0 is a no-op. */
 size_t qoq_kv4_page_bytes(int H_kv, int D, int page_size);
 int qoq_kv4_append(const void* K_fp16, const void* V_fp16, const int32_t* slots, int B, int H_kv, int D,

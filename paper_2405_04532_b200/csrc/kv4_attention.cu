@@ -24,7 +24,8 @@ constexpr int kAttnWarps = 8;
 #ifndef QOQ_KV4_SPLIT
 #define QOQ_KV4_SPLIT 2
 #endif
-constexpr int kAttnSplit = QOQ_KV4_SPLIT;   // CTAs (one thread-block cluster) per (sequence, kv head), merged over DSMEM
+constexpr int kAttnSplit = QOQ_KV4_SPLIT;
+constexpr int kKvStages = 3;    // pages in flight per CTA (TMA bulk copies into shared memory)   // CTAs (one thread-block cluster) per (sequence, kv head), merged over DSMEM
 
 __device__ __forceinline__ size_t kv_head_bytes(int P) { return (size_t)P * (kKvD + 8); }
 
@@ -95,7 +96,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) kv4_decode_attn_kernel(
     pdl_wait();
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
-    const int b = blockIdx.x, g = blockIdx.y, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int b = blockIdx.x, g = blockIdx.y, l = threadIdx.x & 31;
+    // warp index via a lane-0 broadcast: provably warp-uniform, so the token loop (and the shuffles in
+    // it) need no per-shuffle reconvergence code
+    const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     const int rank = (int)cluster.block_rank();           // = blockIdx.z: this CTA's share of the tokens
     const int H = H_kv * R;
     const int T = seq_lens[b];
@@ -119,83 +123,101 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) kv4_decode_attn_kernel(
     const size_t hb = kv_head_bytes(P), pb = (size_t)H_kv * hb;
     const int32_t* bt = block_table + (size_t)b * max_pages;
     const int myc = l / R, myj = l % R;
-    for (int t0 = (rank * kAttnWarps + w) * C; t0 < T; t0 += kAttnSplit * kAttnWarps * C) {
-        // a chunk never crosses a page (t0 % C == 0 and P % C == 0): one block-table lookup, the chunk's
-        // (s, z) pairs as 16-byte broadcast loads; tokens past T read as zeros (masked below)
-        uint32_t kc[C], vc[C], kp[C], vp[C];   // codes (16 bits), (s, z) fp16 pairs
-        {
-            const uint8_t* base = pages + (size_t)__ldg(bt + t0 / P) * pb + (size_t)g * hb;
-            const int o0 = t0 % P;
-            const uint16_t* kcp = reinterpret_cast<const uint16_t*>(base + (size_t)o0 * (kKvD / 2)) + l;
-            const uint16_t* vcp = reinterpret_cast<const uint16_t*>(base + (size_t)(P + o0) * (kKvD / 2)) + l;
-            const uint4* kpp = reinterpret_cast<const uint4*>(base + (size_t)P * kKvD + (size_t)o0 * 4);
-            const uint4* vpp = reinterpret_cast<const uint4*>(base + (size_t)P * kKvD + (size_t)(P + o0) * 4);
+    // TMA pipeline: the (page, kv head) slice — K codes, V codes, (s, z) pairs: P·(D+8) contiguous bytes —
+    // arrives in shared memory by one cp.async.bulk per page, kKvStages pages ahead of the warps.
+    extern __shared__ __align__(16) uint8_t stage_buf[];
+    __shared__ __align__(8) uint64_t full_bar[kKvStages];
+    const int NP = (T + P - 1) / P;                        // pages of this sequence
+    const int my_pages = NP > rank ? (NP - rank + kAttnSplit - 1) / kAttnSplit : 0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kKvStages; ++i) mbar_init(&full_bar[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t policy = policy_evict_first();
+    if (threadIdx.x == 0) {
+        for (int n = 0; n < kKvStages && n < my_pages; ++n) {
+            mbar_arrive_expect_tx(&full_bar[n], (uint32_t)hb);
+            bulk_g2s(stage_buf + (size_t)n * hb, pages + (size_t)__ldg(bt + rank + kAttnSplit * n) * pb + (size_t)g * hb,
+                     (uint32_t)hb, &full_bar[n], policy);
+        }
+    }
+    for (int n = 0; n < my_pages; ++n) {
+        const int stg = n % kKvStages;
+        mbar_wait(&full_bar[stg], (uint32_t)((n / kKvStages) & 1));
+        const uint8_t* base = stage_buf + (size_t)stg * hb;
+        const int tp = (rank + kAttnSplit * n) * P;        // first token of this page
+        for (int o0 = w * C; o0 < P; o0 += kAttnWarps * C) {
+            const int t0 = tp + o0;
+            if (t0 >= T) break;
+            uint32_t kc[C], vc[C], kp[C], vp[C];           // codes (16 bits), (s, z) fp16 pairs
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                kc[c] = __ldg(kcp + c * (kKvD / 4));
-                vc[c] = __ldg(vcp + c * (kKvD / 4));
+                const bool in = t0 + c < T;
+                kc[c] = in ? reinterpret_cast<const uint16_t*>(base + (size_t)(o0 + c) * (kKvD / 2))[l] : 0u;
+                vc[c] = in ? reinterpret_cast<const uint16_t*>(base + (size_t)(P + o0 + c) * (kKvD / 2))[l] : 0u;
+                kp[c] = in ? reinterpret_cast<const uint32_t*>(base + (size_t)P * kKvD)[o0 + c] : 0u;
+                vp[c] = in ? reinterpret_cast<const uint32_t*>(base + (size_t)P * kKvD)[P + o0 + c] : 0u;
             }
+            float v[32];
 #pragma unroll
-            for (int c4 = 0; c4 < C / 4; ++c4) {
-                const uint4 a = __ldg(kpp + c4), bb = __ldg(vpp + c4);
-                kp[4 * c4] = a.x; kp[4 * c4 + 1] = a.y; kp[4 * c4 + 2] = a.z; kp[4 * c4 + 3] = a.w;
-                vp[4 * c4] = bb.x; vp[4 * c4 + 1] = bb.y; vp[4 * c4 + 2] = bb.z; vp[4 * c4 + 3] = bb.w;
+            for (int c = 0; c < C; ++c) {
+                float kh[4];
+                const float2 k2 = __half22float2(*reinterpret_cast<const __half2*>(&kp[c]));
+                dequant4(kc[c], k2.x, -k2.y * k2.x, kh);
+#pragma unroll
+                for (int j = 0; j < R; ++j)
+                    v[c * R + j] = qf[j][0] * kh[0] + qf[j][1] * kh[1] + qf[j][2] * kh[2] + qf[j][3] * kh[3];
             }
+            // butterfly reduce-scatter: lane L ends with the warp sum of v[L]
 #pragma unroll
-            for (int c = 0; c < C; ++c)
-                if (t0 + c >= T) kc[c] = vc[c] = kp[c] = vp[c] = 0u;
-        }
-        float v[32];
+            for (int st = 16; st >= 1; st >>= 1) {
+                const bool up = (l & st) != 0;
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            float kh[4];
-            const float2 k2 = __half22float2(*reinterpret_cast<const __half2*>(&kp[c]));
-            dequant4(kc[c], k2.x, -k2.y * k2.x, kh);
-#pragma unroll
-            for (int j = 0; j < R; ++j)
-                v[c * R + j] = qf[j][0] * kh[0] + qf[j][1] * kh[1] + qf[j][2] * kh[2] + qf[j][3] * kh[3];
-        }
-        // butterfly reduce-scatter: lane L ends with the warp sum of v[L]
-#pragma unroll
-        for (int st = 16; st >= 1; st >>= 1) {
-            const bool up = (l & st) != 0;
-#pragma unroll
-            for (int i = 0; i < st; ++i) {
-                const float send = up ? v[i] : v[i + st];
-                const float keep = up ? v[i + st] : v[i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+                for (int i = 0; i < st; ++i) {
+                    const float send = up ? v[i] : v[i + st];
+                    const float keep = up ? v[i + st] : v[i];
+                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+                }
             }
-        }
-        const float sc = (t0 + myc < T) ? v[0] : -INFINITY;
-        float cm = sc;                                          // chunk max over the lanes of head myj
+            const float sc = (t0 + myc < T) ? v[0] : -INFINITY;
+            float cm = sc;                                          // chunk max over the lanes of head myj
 #pragma unroll
-        for (int x = R; x < 32; x <<= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, x));
-        float mj = m[0];
+            for (int x = R; x < 32; x <<= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, x));
+            float mj = m[0];
 #pragma unroll
-        for (int j = 1; j < R; ++j) mj = (myj == j) ? m[j] : mj;
-        const float mnew = fmaxf(mj, cm);
-        const float p = (sc == -INFINITY) ? 0.0f : exp2f(sc - mnew);
-        const float corr = (mj == -INFINITY) ? 0.0f : exp2f(mj - mnew);
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            const float cj = __shfl_sync(0xffffffffu, corr, j);
-            m[j] = __shfl_sync(0xffffffffu, mnew, j);
-            lsum[j] *= cj;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[j][i] *= cj;
-        }
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            float vh[4];
-            const float2 v2 = __half22float2(*reinterpret_cast<const __half2*>(&vp[c]));
-            dequant4(vc[c], v2.x, -v2.y * v2.x, vh);
+            for (int j = 1; j < R; ++j) mj = (myj == j) ? m[j] : mj;
+            const float mnew = fmaxf(mj, cm);
+            const float p = (sc == -INFINITY) ? 0.0f : exp2f(sc - mnew);
+            const float corr = (mj == -INFINITY) ? 0.0f : exp2f(mj - mnew);
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-                const float pc = __shfl_sync(0xffffffffu, p, c * R + j);
-                lsum[j] += pc;
+                const float cj = __shfl_sync(0xffffffffu, corr, j);
+                m[j] = __shfl_sync(0xffffffffu, mnew, j);
+                lsum[j] *= cj;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) acc[j][i] = __fmaf_rn(pc, vh[i], acc[j][i]);
+                for (int i = 0; i < 4; ++i) acc[j][i] *= cj;
             }
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                float vh[4];
+                const float2 v2 = __half22float2(*reinterpret_cast<const __half2*>(&vp[c]));
+                dequant4(vc[c], v2.x, -v2.y * v2.x, vh);
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const float pc = __shfl_sync(0xffffffffu, p, c * R + j);
+                    lsum[j] += pc;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[j][i] = __fmaf_rn(pc, vh[i], acc[j][i]);
+                }
+            }
+        }
+        __syncthreads();                                   // every warp is done with stage stg
+        if (threadIdx.x == 0 && n + kKvStages < my_pages) {
+            mbar_arrive_expect_tx(&full_bar[stg], (uint32_t)hb);
+            bulk_g2s(stage_buf + (size_t)stg * hb,
+                     pages + (size_t)__ldg(bt + rank + kAttnSplit * (n + kKvStages)) * pb + (size_t)g * hb,
+                     (uint32_t)hb, &full_bar[stg], policy);
         }
     }
     // merge the 8 warps' partial softmax states
@@ -258,6 +280,7 @@ cudaError_t launch_kv4_decode_attention(const void* Q, const uint8_t* pages, con
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(B, H_kv, kAttnSplit);
     cfg.blockDim = dim3(kAttnWarps * 32);
+    cfg.dynamicSmemBytes = (size_t)kKvStages * P * (kKvD + 8);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -268,6 +291,17 @@ cudaError_t launch_kv4_decode_attention(const void* Q, const uint8_t* pages, con
     cfg.numAttrs = 1;
     const __half* q = static_cast<const __half*>(Q);
     __half* o = static_cast<__half*>(O);
+    {   // static (merge buffers) + dynamic (page stages) may exceed the default 48 KB: opt in
+        cudaError_t e = cudaSuccess;
+        switch (H / H_kv) {
+            case 1: e = cudaFuncSetAttribute(kv4_decode_attn_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes); break;
+            case 2: e = cudaFuncSetAttribute(kv4_decode_attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes); break;
+            case 4: e = cudaFuncSetAttribute(kv4_decode_attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes); break;
+            case 8: e = cudaFuncSetAttribute(kv4_decode_attn_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes); break;
+            default: return cudaErrorInvalidValue;
+        }
+        if (e != cudaSuccess) return e;
+    }
     switch (H / H_kv) {
         case 1: return cudaLaunchKernelEx(&cfg, kv4_decode_attn_kernel<1>, q, pages, block_table, seq_lens, H_kv, P, max_pages, o);
         case 2: return cudaLaunchKernelEx(&cfg, kv4_decode_attn_kernel<2>, q, pages, block_table, seq_lens, H_kv, P, max_pages, o);

@@ -209,7 +209,7 @@ int kv4_shape_status(int B, int H, int H_kv, int D, int P) {
     if (H % H_kv) return QOQ_ERR_SHAPE;
     const int r = H / H_kv;
     if (r != 1 && r != 2 && r != 4 && r != 8) return QOQ_ERR_UNSUPPORTED;
-    if (P % 32) return QOQ_ERR_UNSUPPORTED;   // token chunks of 32 / r never cross a page
+    if (P % 32 || P > 256) return QOQ_ERR_UNSUPPORTED;   // 32/r-token chunks within a page; 3 page stages in smem
     return QOQ_OK;
 }
 }  // namespace
