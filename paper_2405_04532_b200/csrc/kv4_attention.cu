@@ -25,7 +25,10 @@ constexpr int kAttnWarps = 8;
 #define QOQ_KV4_SPLIT 2
 #endif
 constexpr int kAttnSplit = QOQ_KV4_SPLIT;
-constexpr int kKvStages = 3;    // pages in flight per CTA (TMA bulk copies into shared memory)   // CTAs (one thread-block cluster) per (sequence, kv head), merged over DSMEM
+#ifndef QOQ_KV4_STAGES
+#define QOQ_KV4_STAGES 3
+#endif
+constexpr int kKvStages = QOQ_KV4_STAGES;    // pages in flight per CTA (TMA bulk copies into shared memory)   // CTAs (one thread-block cluster) per (sequence, kv head), merged over DSMEM
 
 __device__ __forceinline__ size_t kv_head_bytes(int P) { return (size_t)P * (kKvD + 8); }
 
