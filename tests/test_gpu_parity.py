@@ -312,8 +312,11 @@ def _fused_case(M, N, K, ldx, seed):
     return X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref
 
 
-@pytest.mark.parametrize("path", ["fused", "two"])
-@pytest.mark.parametrize("mode", ["auto", "0", "1", "2", "cg2"])
+# the two-kernel path is covered by the GEMM parity tests; auto / 2 suffice for it here
+PATH_MODES = [("fused", m) for m in ("auto", "0", "1", "2", "cg2")] + [("two", "auto"), ("two", "2")]
+
+
+@pytest.mark.parametrize("path,mode", PATH_MODES)
 @pytest.mark.parametrize("M,N,K,ldx", FUSED_SHAPES)
 def test_fused_linear_bit_exact(gpu_lib, monkeypatch, path, mode, M, N, K, ldx):
     """qoq_w4a8_linear, on the fused path (QOQ_LINEAR_FUSED=1: per-token quantization inside the
@@ -325,8 +328,6 @@ def test_fused_linear_bit_exact(gpu_lib, monkeypatch, path, mode, M, N, K, ldx):
         monkeypatch.setenv("QOQ_LINEAR_FUSED", "1")
     else:
         monkeypatch.delenv("QOQ_LINEAR_FUSED", raising=False)
-    if path == "two" and mode not in ("auto", "2"):
-        pytest.skip("the two-kernel path is covered by the GEMM parity tests; auto/2 suffice here")
     if mode == "cg2":
         monkeypatch.setenv("QOQ_FORCE_CG", "2")
     elif mode != "auto":
