@@ -84,3 +84,25 @@ def tp_linear(X, W_shard, kind: str, linear, all_reduce, rank: int, world: int):
     if kind == "row" and world > 1:
         all_reduce(Y)
     return Y
+
+
+def gate_up_shard_rows(I: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows of gate (and of up) a rank holds in the fused column-parallel gate_up weight [2I][K]: its
+    shard is [gate[a:b]; up[a:b]], so its output is [gate_r | up_r] and SiLU(gate)·up stays rank-local."""
+    if I % (GROUP * world):
+        raise ValueError(f"intermediate size {I} not divisible into {world} shards of 128-multiples")
+    return shard_bounds(I, rank, world)
+
+
+def tp_mlp(X, gate_up_shard, down_shard, linear, act_linear, all_reduce, rank: int, world: int):
+    """The TP FFN of Fig. 7 on this rank: column-parallel gate_up (no collective), SiLU(gate)·up on the
+    rank's [gate_r | up_r] with the per-token quantization fused in (NEXT-2; per-rank scales over the
+    I-shard, reading Q17), row-parallel down, ONE all-reduce.
+
+    linear(X, W_shard) -> fp16 Y (quantize X per token + W4A8 GEMM)
+    act_linear(GU_r, W_shard) -> fp16 partial of down (silu_mul_quantize of GU_r + W4A8 GEMM)"""
+    GU_r = linear(X, gate_up_shard)
+    Y = act_linear(GU_r, down_shard)
+    if world > 1:
+        all_reduce(Y)
+    return Y

@@ -144,3 +144,80 @@ def test_packed_row_shards_sum_to_the_full_accumulator():
         qx_r = np.ascontiguousarray(parallel.shard_input(qx, "row", r, 3))
         tot += oracle.acc_from_packed(qx_r, p_r, N, K // 3)
     assert np.array_equal(tot, full)
+
+
+# ---- TP FFN with the SiLU·mul quantization fused (NEXT-2) over gloo ----
+
+def _mlp_weights(I, K):
+    Wg = synth.weights_fp16(I, K, seed=7, std_scale=0.25)
+    Wu = synth.weights_fp16(I, K, seed=8, std_scale=0.25)
+    Wd = synth.weights_fp16(K, I, seed=9, std_scale=0.25)
+    return Wg, Wu, Wd
+
+
+def _mlp_oracle_act_linear(GU_r, shard):
+    """silu_mul_quantize of [gate_r | up_r] (oracle, Q23) + the W4A8 GEMM of the down shard."""
+    packed, s0, N = shard
+    GU = GU_r.numpy() if hasattr(GU_r, "numpy") else GU_r
+    qx, sx, tx = oracle.silu_mul_quantize(np.ascontiguousarray(GU))
+    acc = oracle.acc_from_packed(qx, np.ascontiguousarray(packed), N, qx.shape[1])
+    y = oracle.epilogue_f64(acc, sx, np.ascontiguousarray(s0))
+    return torch.from_numpy(y.astype(np.float16))
+
+
+def _mlp_worker(rank, world, port, M, I, K, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        Wg, Wu, Wd = _mlp_weights(I, K)
+        X = synth.activations_fp16(M, K, seed=7)
+        a, b = parallel.gate_up_shard_rows(I, rank, world)
+        gu = np.ascontiguousarray(np.concatenate([Wg[a:b], Wu[a:b]], axis=0))
+        p_gu, s_gu = oracle.quantize_weights(gu)
+        p_d, s_d = oracle.quantize_weights(Wd)
+        p_dr, s_dr = parallel.shard_packed(p_d, s_d, K, I, "row", rank, world)
+
+        def all_reduce(Y):
+            dist.all_reduce(Y, op=dist.ReduceOp.SUM)
+
+        GU_r = _oracle_linear(X, (p_gu, s_gu, 2 * (b - a)))
+        Y = parallel.tp_mlp(X, (p_gu, s_gu, 2 * (b - a)), (p_dr, s_dr, K), _oracle_linear,
+                            _mlp_oracle_act_linear, all_reduce, rank, world)
+        out_q.put((rank, (GU_r.numpy(), Y.numpy())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp_mlp_gloo_fused_silu_quant():
+    """TP FFN (world 2): each rank's [gate_r | up_r] equals the 1-GPU gate / up outputs on its rows (bit
+    for bit: column-parallel), SiLU·mul + quantization stays rank-local on that pair, and the all-reduced
+    down output matches the fp64 sum of the per-rank exact partials within tolerance."""
+    M, I, K, world = 4, 256, 256, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mlp_worker, args=(r, world, port, M, I, K, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    Wg, Wu, Wd = _mlp_weights(I, K)
+    X = synth.activations_fp16(M, K, seed=7)
+    gate = _oracle_linear(X, (*oracle.quantize_weights(Wg), I)).numpy()
+    up = _oracle_linear(X, (*oracle.quantize_weights(Wu), I)).numpy()
+    ref = np.zeros((M, K))
+    for r in range(world):
+        a, b = parallel.gate_up_shard_rows(I, r, world)
+        GU_r = res[r][0]
+        assert np.array_equal(GU_r[:, : b - a].view(np.uint16), gate[:, a:b].view(np.uint16))
+        assert np.array_equal(GU_r[:, b - a:].view(np.uint16), up[:, a:b].view(np.uint16))
+        p_d, s_d = oracle.quantize_weights(Wd)
+        p_dr, s_dr = parallel.shard_packed(p_d, s_d, K, I, "row", r, world)
+        qx, sx, _ = oracle.silu_mul_quantize(np.ascontiguousarray(GU_r))
+        ref += oracle.epilogue_f64(oracle.acc_from_packed(qx, p_dr, K, I // world), sx, s_dr)
+    assert np.array_equal(res[0][1].view(np.uint16), res[1][1].view(np.uint16))   # all ranks agree
+    y = res[0][1].astype(np.float64)
+    assert np.all(np.abs(y - ref) <= RTOL * np.abs(ref) + ATOL)
