@@ -451,8 +451,10 @@ def main():
 
     # ---- e2e through the C ABI with host buffers (H2D + quantize + GEMM + D2H per GEMM)
     if not args.no_e2e:
+        # N > 1: one stream, so every rank issues its all-reduces in one order (collectives spread over
+        # several streams may interleave differently across ranks and deadlock)
         line["e2e"] = e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stream, step_bytes,
-                                  nstreams=args.e2e_streams)
+                                  nstreams=args.e2e_streams if world == 1 else 1)
 
     if not args.no_prefill:
         line["prefill"] = prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream)
