@@ -25,7 +25,7 @@ def kv_rows(T, H_kv, seed, scale=1.0):
     return x.astype(np.float16)
 
 
-def oracle_cache(Ks, Vs, tables, n_pages):
+def oracle_cache(Ks, Vs, tables, n_pages, P=P):
     """Ks/Vs: per sequence [T][H_kv][D] fp16 -> (pages, [(Khat, Vhat)])."""
     H_kv = Ks[0].shape[1]
     pages = np.zeros(n_pages * oracle.kv4_page_bytes(H_kv, D, P), np.uint8)
@@ -43,7 +43,7 @@ def oracle_cache(Ks, Vs, tables, n_pages):
     return pages, deq
 
 
-def tables_for(lens, seed):
+def tables_for(lens, seed, P=P):
     need = [max(1, -(-T // P)) for T in lens]
     n_pages = sum(need) + 3
     perm = np.random.default_rng(seed).permutation(n_pages)
@@ -77,12 +77,12 @@ def test_kv4_append_pages_byte_exact(gpu_lib, B, H_kv, T):
     assert bad.size == 0, f"{bad.size} page bytes differ, first at {bad[:8].tolist()}"
 
 
-def check_attention(gpu_lib, lens, H, H_kv, seed):
+def check_attention(gpu_lib, lens, H, H_kv, seed, P=P):
     B = len(lens)
-    bt, n_pages = tables_for(lens, seed)
+    bt, n_pages = tables_for(lens, seed, P)
     Ks = [kv_rows(T, H_kv, seed + 100 + b) for b, T in enumerate(lens)]
     Vs = [kv_rows(T, H_kv, seed + 200 + b, scale=0.7) for b, T in enumerate(lens)]
-    pages, deq = oracle_cache(Ks, Vs, bt, n_pages)
+    pages, deq = oracle_cache(Ks, Vs, bt, n_pages, P)
     Q = (synth.normal(seed, 6, B * H * D).reshape(B, H, D) * 2.0).astype(np.float16)
     O = gpu_lib.kv4_decode_attention(to_dev(Q), to_dev(pages), to_dev(bt), to_dev(np.array(lens, np.int32)),
                                      H_kv, P)
@@ -126,3 +126,10 @@ def test_kv4_attention_bench_size_sampled(gpu_lib):
         Kh, Vh = deq[b]
         ref = oracle.attention_f64(Q[b], Kh, Vh)
         assert np.all(np.abs(o[b] - ref) <= 2e-3 * np.abs(ref) + 2e-3 * np.abs(Vh).max()), b
+
+
+@pytest.mark.parametrize("page", [32, 256])
+def test_kv4_attention_page_sizes(gpu_lib, page):
+    """Other page sizes: 32 (the smallest allowed) and 256 (the largest: 3 staged pages of 34.8 KB in
+    shared memory, past the default 48 KB)."""
+    check_attention(gpu_lib, [1, page - 1, page, page + 1, 3 * page + 5], 32, 8, seed=page, P=page)
