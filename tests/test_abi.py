@@ -141,6 +141,7 @@ def test_kv4_validation(lib):
     assert lib.qoq_kv4_append(fake, fake, None, 4, 8, 128, 64, fake, None) == 1           # slots missing
     assert lib.qoq_kv4_append(fake, fake, fake, 0, 8, 128, 64, fake, None) == 0
     assert lib.qoq_kv4_append(fake, fake, fake, 4, 8, 128, 48, fake, None) == 3            # page_size % 32
+    assert lib.qoq_kv4_append(fake, fake, fake, 4, 8, 128, 512, fake, None) == 3           # page_size > 256
     args = (fake, fake, fake, fake, 4, 32, 8, 128, 64, 16, fake, None)
     assert lib.qoq_kv4_decode_attention(fake, fake, fake, fake, 4, 30, 8, 128, 64, 16, fake, None) == 2
     assert lib.qoq_kv4_decode_attention(fake, fake, fake, fake, 4, 48, 3, 128, 64, 16, fake, None) == 3
