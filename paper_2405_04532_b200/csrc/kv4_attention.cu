@@ -25,6 +25,9 @@ constexpr int kAttnWarps = 8;
 #define QOQ_KV4_SPLIT 2
 #endif
 constexpr int kAttnSplit = QOQ_KV4_SPLIT;
+#ifndef QOQ_KV4_MINB
+#define QOQ_KV4_MINB 2   // CTAs per SM the register budget is sized for
+#endif
 #ifndef QOQ_KV4_STAGES
 #define QOQ_KV4_STAGES 3
 #endif
@@ -90,7 +93,7 @@ __device__ __forceinline__ void dequant4(uint32_t c, float s, float zs, float (&
 // The chunk's softmax update runs on those lanes (max over the lanes of one head, one exp2 each), the
 // 32 probabilities are broadcast back by shuffles and the lane accumulates p · v̂ for its 4 dims.
 template <int R>
-__global__ void __launch_bounds__(kAttnWarps * 32, 2) kv4_decode_attn_kernel(
+__global__ void __launch_bounds__(kAttnWarps * 32, QOQ_KV4_MINB) kv4_decode_attn_kernel(
     const __half* __restrict__ Q, const uint8_t* __restrict__ pages, const int32_t* __restrict__ block_table,
     const int32_t* __restrict__ seq_lens, int H_kv, int P, int max_pages, __half* __restrict__ O) {
     constexpr int C = 32 / R;
