@@ -227,7 +227,13 @@ def kv4_append(K: torch.Tensor, V: torch.Tensor, slots: torch.Tensor, pages: tor
                stream=None):
     """Quantize one new token per sequence into the KV4 page pool (NEXT-4; C-ABI qoq_kv4_append).
     K, V [B][H_kv][D] fp16; slots [B] int32 (page * page_size + offset); pages uint8 pool."""
+    if K.dim() != 3 or K.shape != V.shape or K.dtype != torch.float16 or V.dtype != torch.float16:
+        raise ValueError("K and V must be [B][H_kv][D] fp16 tensors of the same shape")
     B, H_kv, D = K.shape
+    if slots.dtype != torch.int32 or slots.numel() != B:
+        raise ValueError("slots must be int32 [B]")
+    if pages.dtype != torch.uint8:
+        raise ValueError("pages must be a uint8 tensor")
     _check("qoq_kv4_append", load().qoq_kv4_append(_ptr(K), _ptr(V), _ptr(slots), B, H_kv, D, page_size,
                                                    _ptr(pages), _stream(stream)))
 
@@ -236,8 +242,18 @@ def kv4_decode_attention(Q: torch.Tensor, pages: torch.Tensor, block_table: torc
                          H_kv: int, page_size: int = 64, out=None, stream=None):
     """Decode attention over the KV4 cache (§5.3; C-ABI qoq_kv4_decode_attention): Q [B][H][D] fp16 ->
     O [B][H][D] fp16."""
+    if Q.dim() != 3 or Q.dtype != torch.float16:
+        raise ValueError("Q must be a [B][H][D] fp16 tensor")
     B, H, D = Q.shape
+    if pages.dtype != torch.uint8:
+        raise ValueError("pages must be a uint8 tensor")
+    if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.shape[0] != B:
+        raise ValueError("block_table must be int32 [B][max_pages]")
+    if seq_lens.dtype != torch.int32 or seq_lens.numel() != B:
+        raise ValueError("seq_lens must be int32 [B]")
     O = torch.empty_like(Q) if out is None else out
+    if O.shape != Q.shape or O.dtype != torch.float16:
+        raise ValueError("out must be fp16 with Q's shape")
     _check("qoq_kv4_decode_attention",
            load().qoq_kv4_decode_attention(_ptr(Q), _ptr(pages), _ptr(block_table), _ptr(seq_lens), B, H, H_kv,
                                            D, page_size, block_table.shape[1], _ptr(O), _stream(stream)))
@@ -247,30 +263,37 @@ def kv4_decode_attention(Q: torch.Tensor, pages: torch.Tensor, block_table: torc
 class Workspace:
     """Zero-filled workspace that grows on demand. A GEMM workspace is left zeroed by the library; a
     linear (w4a8_linear) workspace additionally holds the last call's q_x / s_x / t_x, so do not pass
-    the same Workspace to both kinds of call."""
+    the same Workspace to both kinds of call, nor to concurrent calls on different streams."""
 
     def __init__(self, device=None):
         self.device = device
         self.buf = None
 
-    def get(self, nbytes: int):
+    def get(self, nbytes: int, stream=None):
+        """The buffer (grown and zero-filled on `stream`, the stream the call launches on)."""
         if nbytes == 0:
             return None, 0
         if self.buf is None or self.buf.numel() < nbytes:
-            self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device or "cuda")
+            s = torch.cuda.current_stream(self.device) if stream is None else stream
+            with torch.cuda.stream(s):
+                self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device or "cuda")
         return self.buf, self.buf.numel()
 
 
 _default_ws: dict = {}
 
 
-def _ws_for(device, nbytes, workspace, kind="gemm"):
-    """Default workspaces are per (device, stream, kind): a GEMM workspace must stay all-zero between
-    calls, while a linear workspace also holds the call's quantized activations, so the two kinds
-    never share a buffer."""
+def _ws_for(device, nbytes, workspace, kind="gemm", stream=None):
+    """Default workspaces are per (device, LAUNCH stream, kind): calls on different streams never share
+    one (a GEMM workspace holds split-K partials and tile counters that must be zero on entry), and it
+    is allocated and zero-filled on the stream the kernel runs on. A linear workspace also holds the
+    call's quantized activations, so the two kinds never share a buffer."""
+    s = torch.cuda.current_stream(device) if stream is None else stream
     if workspace is None:
-        key = (str(device), torch.cuda.current_stream(device).cuda_stream, kind)
+        key = (str(device), s.cuda_stream, kind)
         workspace = _default_ws.setdefault(key, Workspace(device))
+    if isinstance(workspace, Workspace):
+        return workspace.get(nbytes, s)
     return workspace.get(nbytes)
 
 
@@ -280,7 +303,7 @@ def w4a8_gemm(qx: torch.Tensor, sx: torch.Tensor, tx: torch.Tensor | None, packe
     """Y [M][N] fp16 = fp16(s_x[m] s0[n] Σ_k qx[m][k] q̂[n][k])."""
     M, K = qx.shape
     Y = torch.empty(M, N, dtype=torch.float16, device=qx.device) if out is None else out
-    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace)
+    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace, stream=stream)
     _check("qoq_w4a8_gemm",
            load().qoq_w4a8_gemm(_ptr(qx), _ptr(sx), _ptr(tx), _ptr(packed), _ptr(s0), M, N, K, GROUP,
                                 _ptr(Y), Y.stride(0), _ptr(ws), wsb, _stream(stream)))
@@ -292,7 +315,7 @@ def w4a8_gemm_i32(qx: torch.Tensor, tx: torch.Tensor | None, packed: torch.Tenso
     """Exact INT32 accumulators acc [M][N] (parity/debug entry)."""
     M, K = qx.shape
     acc = torch.empty(M, N, dtype=torch.int32, device=qx.device)
-    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace)
+    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace, stream=stream)
     _check("qoq_w4a8_gemm_i32",
            load().qoq_w4a8_gemm_i32(_ptr(qx), _ptr(tx), _ptr(packed), M, N, K, GROUP, _ptr(acc), N,
                                     _ptr(ws), wsb, _stream(stream)))
@@ -308,7 +331,7 @@ def w4a8_linear(X: torch.Tensor, packed: torch.Tensor, s0: torch.Tensor, N: int,
     M, ldx = X.shape
     K = ldx if K is None else K
     Y = torch.empty(M, N, dtype=torch.float16, device=X.device) if out is None else out
-    ws, wsb = _ws_for(X.device, linear_workspace_bytes(M, N, K), workspace, kind="linear")
+    ws, wsb = _ws_for(X.device, linear_workspace_bytes(M, N, K), workspace, kind="linear", stream=stream)
     _check("qoq_w4a8_linear",
            load().qoq_w4a8_linear(_ptr(X), ldx, M, N, K, GROUP, _ptr(packed), _ptr(s0), _ptr(Y), Y.stride(0),
                                   _ptr(ws), wsb, _stream(stream)))
@@ -360,7 +383,7 @@ def pc_w4a8_gemm(qx: torch.Tensor, sx: torch.Tensor, tx: torch.Tensor, packed: t
     """Y [M][N] fp16 = fp16(s_x[m] s_w[n] (Σ_k qx q_u4 − z_w[n] t_x[m]))."""
     M, K = qx.shape
     Y = torch.empty(M, N, dtype=torch.float16, device=qx.device) if out is None else out
-    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace)
+    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace, stream=stream)
     _check("qoq_pc_w4a8_gemm",
            load().qoq_pc_w4a8_gemm(_ptr(qx), _ptr(sx), _ptr(tx), _ptr(packed), _ptr(s_w), _ptr(z_w), M, N, K,
                                    _ptr(Y), Y.stride(0), _ptr(ws), wsb, _stream(stream)))
@@ -372,7 +395,7 @@ def pc_w4a8_gemm_i32(qx: torch.Tensor, tx: torch.Tensor, packed: torch.Tensor, z
     """Exact INT32 Σ_k qx (q_u4 − z_w) [M][N] (parity entry)."""
     M, K = qx.shape
     acc = torch.empty(M, N, dtype=torch.int32, device=qx.device)
-    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace)
+    ws, wsb = _ws_for(qx.device, gemm_workspace_bytes(M, N, K), workspace, stream=stream)
     _check("qoq_pc_w4a8_gemm_i32",
            load().qoq_pc_w4a8_gemm_i32(_ptr(qx), _ptr(tx), _ptr(packed), _ptr(z_w), M, N, K, _ptr(acc), N,
                                        _ptr(ws), wsb, _stream(stream)))

@@ -384,3 +384,24 @@ def test_fused_linear_in_cuda_graph(gpu_lib, monkeypatch, path):
         g.replay()
         torch.cuda.synchronize()
         check_y(Y, oracle.linear_rows(X, p_ref, s0_ref, N))
+
+
+def test_default_workspace_per_launch_stream(gpu_lib, monkeypatch):
+    """the default workspace is keyed by the stream the call LAUNCHES on (not torch's
+    current stream). Stream-K GEMMs (mode 1: split-K partials and tile counters in the workspace,
+    zero on entry) issued back to back on two explicit streams, with no ordering between them, must
+    each give the exact accumulators."""
+    monkeypatch.setenv("QOQ_FORCE_MODE", "1")
+    M, N, K = 64, 1280, 3200
+    W, X, p_ref, s0_ref, qx_ref, sx_ref, tx_ref = _case(M, N, K, seed=91)
+    acc_ref = oracle.acc_from_packed(qx_ref, p_ref, N, K)
+    qx, tx, packed = to_dev(qx_ref), to_dev(tx_ref), to_dev(p_ref)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(8):
+        outs.append(gpu_lib.w4a8_gemm_i32(qx, tx, packed, N, stream=s1))
+        outs.append(gpu_lib.w4a8_gemm_i32(qx, tx, packed, N, stream=s2))
+    torch.cuda.synchronize()
+    for a in outs:
+        assert np.array_equal(a.cpu().numpy(), acc_ref)

@@ -112,3 +112,37 @@ def test_kv4_page_layout_by_hand():
     base = 2 * pb + 1 * (D // 2)
     assert pages[base + 2] == qk[t, h, 4] | (qk[t, h, 5] << 4)
     assert np.count_nonzero(pages[pb: 2 * pb]) == 0          # page 1 is not in the table
+
+
+def test_kv4_tolerance_sees_a_missing_token():
+    """Negative control for the GPU attention tolerance (tests/kv4_tol.py, derived from the kernel's
+    fp32 arithmetic): on the bench-shaped data (T = 1024, H = 32, H_kv = 8, an x8 outlier channel) the
+    fp16-rounded exact output passes it, while the oracle with ONE token dropped fails it — for the
+    last token, the first, tokens at the page and page-ring boundaries (63/64, 191/192, 383/384) and a
+    seeded sample (all 1024 single-token drops fail; measured once, 2 min). Also at T = 777 (ragged)
+    dropping the last token, i.e. attending over T - 1, fails it."""
+    import synth
+    from kv4_tol import kv4_tolerance
+    D, H, H_kv = 128, 32, 8
+
+    def rows(T, seed, scale):
+        x = synth.normal(seed, 5, T * H_kv * D).reshape(T, H_kv, D) * scale
+        x[:, :, 3] *= 8.0
+        return x.astype(np.float16)
+
+    for T, sample in ((1024, [0, 1, 63, 64, 191, 192, 383, 384, 1022, 1023]
+                       + list(rng(11).choice(1024, 12, replace=False))), (777, [776])):
+        k = oracle.kv4_quantize(rows(T, 300, 1.0).reshape(-1, D))
+        v = oracle.kv4_quantize(rows(T, 400, 0.7).reshape(-1, D))
+        Kh = oracle.kv4_dequant(*k).reshape(T, H_kv, D)
+        Vh = oracle.kv4_dequant(*v).reshape(T, H_kv, D)
+        Q = (synth.normal(9, 6, H * D).reshape(H, D) * 2.0).astype(np.float16)
+        ref = oracle.attention_f64(Q, Kh, Vh)
+        tol = kv4_tolerance(Q, Kh, Vh, ref)
+        assert np.all(np.abs(ref.astype(np.float16).astype(np.float64) - ref) <= tol)
+        old = 2e-3 * np.abs(ref) + 2e-3 * np.abs(Vh).max()                  # the round-1 bound
+        assert np.median(tol) < np.median(old) / 50
+        for t in sample:
+            keep = np.r_[0:t, t + 1:T]
+            o = oracle.attention_f64(Q, Kh[keep], Vh[keep])
+            assert not np.all(np.abs(o - ref) <= tol), f"dropping token {t} of {T} passes the tolerance"

@@ -449,3 +449,37 @@ def test_pc_linear_approximates_float_gemm():
     ref = X.astype(np.float64) @ W.astype(np.float64).T
     rel = np.linalg.norm(y - ref) / np.linalg.norm(ref)
     assert 0.02 < rel < 0.35, rel
+
+
+# ------------------------------------------------------------------ Q1 tie rule
+
+def test_level1_real_valued_ties_round_half_away():
+    """Q1 (Eq. 2 P:115 ⌈·⌋; P:257's ⌈120/16 + 7⌋ = 15 rules out half-even): level 1 rounds an
+    exact half AWAY from zero. The row max 119·2^-7 gives s0 = 2^-7 exactly, so W = (k + 1/2)·2^-7
+    lands on W/s0 = k + 0.5 in fp32 with no rounding: 2.5 -> 3 (half-even 2), -2.5 -> -3,
+    0.5 -> 1 (half-even 0), -0.5 -> -1, 1.5 -> 2, 118.5 -> 119."""
+    halves = np.array([2.5, -2.5, 0.5, -0.5, 1.5, -1.5, 118.5, -118.5, 3.5, 4.5])
+    W = np.zeros((1, 128), np.float16)
+    W[0, 0] = 119 / 128
+    W[0, 1:1 + len(halves)] = (halves / 128).astype(np.float16)
+    assert np.array_equal(W[0, 1:1 + len(halves)].astype(np.float64) * 128, halves)   # exact in fp16
+    q8, s0 = oracle.level1(W)
+    assert s0[0] == np.float16(2.0 ** -7)
+    assert list(q8[0, 1:1 + len(halves)]) == [3, -3, 1, -1, 2, -2, 119, -119, 4, 5]
+
+
+def test_activations_real_valued_ties_round_half_away():
+    """Q1 for O4: with the row max 127·2^-6 the scale is s_x = 2^-6 exactly and
+    x = (k + 1/2)·2^-6 gives x/s_x = k + 0.5: 2.5 -> 3, -2.5 -> -3, 0.5 -> 1, 126.5 -> 127; t_x
+    sums the half-away codes."""
+    halves = np.array([2.5, -2.5, 0.5, -0.5, 126.5, -126.5, 5.5, -7.5])
+    X = np.zeros((2, 256), np.float16)
+    X[:, 0] = 127 / 64
+    X[0, 1:1 + len(halves)] = (halves / 64).astype(np.float16)
+    X[1, 100:100 + len(halves)] = (-halves / 64).astype(np.float16)
+    qx, sx, tx = oracle.quantize_activations(X)
+    want = [3, -3, 1, -1, 127, -127, 6, -8]
+    assert np.all(sx == np.float16(2.0 ** -6))
+    assert list(qx[0, 1:1 + len(halves)]) == want
+    assert list(qx[1, 100:100 + len(halves)]) == [-w for w in want]
+    assert list(tx) == [127 + sum(want), 127 - sum(want)]
