@@ -40,7 +40,7 @@ typedef enum {
 const char* qoq_status_string(int status);
 /* ABI version of this header (incremented on any signature or layout change). */
 int qoq_abi_version(void);
-#define QOQ_ABI_VERSION 5
+#define QOQ_ABI_VERSION 6
 
 /* ----------------------------------------------------------------------------------------------
  * Packed weight layout (frozen). The B200 form of "store the weights in the order
@@ -117,9 +117,10 @@ int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed,
  * use; each call leaves its synchronization words and split-K partials zeroed again. Layout, each
  * part 256-byte aligned: [256 B sync][GEMM workspace, qoq_gemm_workspace_bytes(M,N,K)]
  * [q_x int8 M*K][s_x fp16 M][t_x int32 M]; after the call q_x / s_x / t_x hold this call's
- * quantized activations. One workspace per stream. Reusing a workspace for another shape is safe
- * when both shapes have the same qoq_gemm_workspace_bytes (the zero-required parts then coincide);
- * otherwise give each shape its own workspace (or re-zero it).
+ * quantized activations. One workspace per stream; it may be reused for any shape: when the GEMM
+ * needs split-K partials (qoq_gemm_workspace_bytes > 0) the call first clears that region with an
+ * async memset on `stream` (it may overlap another shape's q_x), so only the 256 sync bytes must be
+ * zero on entry.
  * Same shape requirements as qoq_w4a8_gemm. */
 size_t qoq_linear_workspace_bytes(int M, int N, int K);
 int qoq_w4a8_linear(const void* X_fp16, int ldx, int M, int N, int K, int group,
@@ -138,6 +139,43 @@ size_t qoq_linear_host_scratch_bytes(int M, int N, int K);
 int qoq_linear_host(const void* X_host_fp16, int M, int K,
                     const void* packed, const void* s0_fp16, int N,
                     void* Y_host_fp16, void* dev_scratch, size_t scratch_bytes, void* stream);
+
+/* ---- Decode chain: n linear layers in ONE persistent launch (ABI v6) ----
+ * The decode-regime form of the whole hot path (SURVEY §8(a) rows a2-a7 for a sequence of linears):
+ * for j = 0 .. n-1, in order, exactly what qoq_w4a8_linear computes,
+ *   Y_j = fp16( (Σ_k q̂_j[n][k] q_x[m][k]) · s_x[m] · s0_j[n] ),  q_x, s_x = per-token INT8 of X_j,
+ * bit-identical to n successive qoq_w4a8_linear calls. Linear j reads X_j only after Y_0..Y_{j-1} are
+ * complete, so X_j may be (a view of) an earlier linear's Y, as in a model. One CTA per SM streams
+ * every linear's packed weights back to back; each linear's K-steps are split over all SMs (stream-K,
+ * P:501) with exact INT32 partial sums reduced in L2; the per-token quantization runs inside the
+ * kernel between linears. DESIGN.md §5.
+ *   desc[j]: X_fp16 [M][ldx] (ldx >= K, ldx % 8 == 0), packed / s0_fp16 as qoq_w4a8_gemm for an [N][K]
+ *            weight, Y_fp16 [M][ldy] (ldy >= N, ldy % 8 == 0). The descriptor array is read on the host
+ *            during the call (the launch captures it by value; it may be freed on return).
+ *   M:       1 .. 128 tokens (the decode regime; above, use the per-GEMM path).
+ *   n:       1 .. 128 linears (one launch; split longer stacks into several chains).
+ *   workspace: qoq_linear_chain_workspace_bytes(M, n, desc) bytes, 256-byte aligned. Only its first
+ *            12288 bytes (grid counters) must be ZERO before the first use; every call leaves them zero
+ *            again, so a workspace can be reused (and graph-replayed) by later calls with any
+ *            descriptors (if large enough), one call at a time. The rest (split-K partial slots, the
+ *            q_x, s_x, t_x) needs no initialization. N <= 65536 and K <= 14336 per linear (else
+ *            QOQ_ERR_SHAPE); at most 16 distinct (K, j % 2) pairs per chain (else QOQ_ERR_UNSUPPORTED).
+ * Requires the whole GPU: the grid is one CTA per SM and all CTAs must be co-resident (grid-wide
+ * release/acquire counters order the linears). Errors: as qoq_w4a8_gemm per descriptor; M or n out of
+ * range -> QOQ_ERR_INVALID_ARG; workspace too small -> QOQ_ERR_WORKSPACE. Launches 1 kernel. */
+typedef struct {
+    const void* X_fp16;
+    int ldx;
+    int N, K;
+    const void* packed;
+    const void* s0_fp16;
+    void* Y_fp16;
+    int ldy;
+} qoq_linear_desc;
+
+size_t qoq_linear_chain_workspace_bytes(int M, int n, const qoq_linear_desc* desc);
+int qoq_w4a8_linear_chain(int M, int n, const qoq_linear_desc* desc, void* workspace, size_t workspace_bytes,
+                          void* stream);
 
 /* ---- Per-channel W4A8 (the paper's other precision mode, §5.2.2; NEXT-1) ----
  * Weights: per-output-channel asymmetric UINT4 (Eq. 2, q_min = 0, q_max = 15) with an
@@ -210,7 +248,8 @@ int qoq_kv4_decode_attention(const void* Q_fp16, const void* pages, const int32_
  * quantize_weights 2, quantize_activations_per_token 1, rmsnorm_quantize 1, silu_mul_quantize 1,
  * kv4_append 1, kv4_decode_attention 1, w4a8_gemm 1, w4a8_gemm_i32 1,
  * pc_quantize_weights 2, pc_w4a8_gemm 1, pc_w4a8_gemm_i32 1,
- * w4a8_linear 2 (1 when fused: QOQ_LINEAR_FUSED=1 and M <= 64), linear_host as w4a8_linear
+ * w4a8_linear 2 (1 when fused: QOQ_LINEAR_FUSED=1 and M <= 64), linear_host as w4a8_linear,
+ * w4a8_linear_chain 1 (for the whole chain)
  * (plus 2 async copies). */
 
 #ifdef __cplusplus

@@ -23,11 +23,12 @@ LIB_PATH = os.path.join(_HERE, "libqoq_b200.so" if not os.environ.get("QOQ_LIB_V
                         else f"libqoq_b200_{os.environ['QOQ_LIB_VARIANT']}.so")
 GROUP = 128
 TILE_BYTES = 8448
-ABI_VERSION = 5
+ABI_VERSION = 6
 # kernels launched per call (matches include/qoq_b200.h)
 LAUNCHES = {"quantize_weights": 2, "quantize_activations_per_token": 1, "w4a8_gemm": 1,
             "w4a8_gemm_i32": 1, "pc_quantize_weights": 2, "pc_w4a8_gemm": 1, "pc_w4a8_gemm_i32": 1,
-            "rmsnorm_quantize": 1, "silu_mul_quantize": 1, "kv4_append": 1, "kv4_decode_attention": 1}
+            "rmsnorm_quantize": 1, "silu_mul_quantize": 1, "kv4_append": 1, "kv4_decode_attention": 1,
+            "w4a8_linear_chain": 1}
 FUSE_MAX_M = 64   # w4a8_linear / linear_host with QOQ_LINEAR_FUSED=1: one fused kernel up to this M
 
 
@@ -82,6 +83,8 @@ def load() -> ctypes.CDLL:
             "qoq_kv4_page_bytes": (Z, [I, I, I]),
             "qoq_kv4_append": (I, [P, P, P, I, I, I, I, P, P]),
             "qoq_kv4_decode_attention": (I, [P, P, P, P, I, I, I, I, I, I, P, P]),
+            "qoq_linear_chain_workspace_bytes": (Z, [I, I, P]),
+            "qoq_w4a8_linear_chain": (I, [I, I, P, P, Z, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -400,3 +403,49 @@ def pc_w4a8_gemm_i32(qx: torch.Tensor, tx: torch.Tensor, packed: torch.Tensor, z
            load().qoq_pc_w4a8_gemm_i32(_ptr(qx), _ptr(tx), _ptr(packed), _ptr(z_w), M, N, K, _ptr(acc), N,
                                        _ptr(ws), wsb, _stream(stream)))
     return acc
+
+
+# ------------------------------------------------------------------ decode chain (one persistent launch)
+
+class LinearDesc(ctypes.Structure):
+    """qoq_linear_desc (include/qoq_b200.h)."""
+    _fields_ = [("X", ctypes.c_void_p), ("ldx", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int),
+                ("packed", ctypes.c_void_p), ("s0", ctypes.c_void_p), ("Y", ctypes.c_void_p), ("ldy", ctypes.c_int)]
+
+
+def chain_descs(layers):
+    """layers: [(X [M][ldx] fp16, packed, s0, N, Y [M][ldy] fp16, K or None)] -> (M, ctypes array)."""
+    M = None
+    arr = (LinearDesc * len(layers))()
+    for i, L in enumerate(layers):
+        X, packed, s0, N, Y = L[:5]
+        K = L[5] if len(L) > 5 and L[5] is not None else X.shape[1]
+        if X.dtype != torch.float16 or Y.dtype != torch.float16 or X.dim() != 2 or Y.dim() != 2:
+            raise ValueError("X and Y must be 2-D fp16 tensors")
+        if X.stride(1) != 1 or Y.stride(1) != 1:
+            raise ValueError("X and Y rows must be contiguous")
+        if M is None:
+            M = X.shape[0]
+        if X.shape[0] != M or Y.shape[0] != M or Y.shape[1] < N:
+            raise ValueError("every linear of a chain takes the same M tokens; Y must be [M][>= N]")
+        arr[i] = LinearDesc(X.data_ptr(), X.stride(0), N, K, _ptr(packed).value, _ptr(s0).value, Y.data_ptr(),
+                            Y.stride(0))
+    return M, arr
+
+
+def linear_chain_workspace_bytes(layers) -> int:
+    M, arr = chain_descs(layers)
+    return load().qoq_linear_chain_workspace_bytes(M, len(arr), arr)
+
+
+def w4a8_linear_chain(layers, workspace: Workspace | None = None, stream=None):
+    """Y_j = w4a8_linear(X_j) for every linear j of `layers`, in order, in ONE persistent kernel (C-ABI
+    qoq_w4a8_linear_chain; M <= 128). X_j may be an earlier Y_i (read after it is complete).
+    layers: [(X, packed, s0, N, Y[, K])]."""
+    M, arr = chain_descs(layers)
+    nbytes = load().qoq_linear_chain_workspace_bytes(M, len(arr), arr)
+    if nbytes == 0:
+        raise ValueError("unsupported chain (M must be 1..128, n 1..128, shapes multiples of 128, K <= 14336)")
+    dev = layers[0][0].device
+    ws, wsb = _ws_for(dev, nbytes, workspace, kind="chain", stream=stream)
+    _check("qoq_w4a8_linear_chain", load().qoq_w4a8_linear_chain(M, len(arr), arr, _ptr(ws), wsb, _stream(stream)))

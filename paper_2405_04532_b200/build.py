@@ -12,8 +12,8 @@ LIB = os.path.join(HERE, "libqoq_b200.so")
 
 def lib_path(variant: str = "") -> str:
     return LIB if not variant else os.path.join(HERE, f"libqoq_b200_{variant}.so")
-SOURCES = ["qoq_api.cu", "quantize.cu", "fused_quant.cu", "kv4_attention.cu", "w4a8_gemm.cu"]
-HEADERS = ["qoq_internal.h", "sm100_ptx.cuh", "qoq_quant.cuh", os.path.join("..", "..", "include", "qoq_b200.h")]
+SOURCES = ["qoq_api.cu", "quantize.cu", "fused_quant.cu", "kv4_attention.cu", "w4a8_gemm.cu", "w4a8_chain.cu"]
+HEADERS = ["qoq_internal.h", "sm100_ptx.cuh", "qoq_quant.cuh", "w4a8_common.cuh", os.path.join("..", "..", "include", "qoq_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-cudart", "static", "--expt-relaxed-constexpr"]

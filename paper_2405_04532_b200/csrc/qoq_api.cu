@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
+#include <memory>
 
 #include "../../include/qoq_b200.h"
 #include "qoq_internal.h"
@@ -106,6 +108,9 @@ int run_linear(const void* X, int ldx, int M, int N, int K, int group, const voi
     // QOQ_LINEAR_FUSED=1 selects the one-kernel path for M <= kFuseMaxM.
     const char* ff = getenv("QOQ_LINEAR_FUSED");
     const bool fused = ff && atoi(ff) == 1;
+    // the split-K region must be zero on entry; in a workspace shared by several shapes it may overlap
+    // another shape's q_x, so the call clears it itself (mode-1 plans only: none at decode sizes)
+    if (w.gemm_ws_bytes > 0 && cudaMemsetAsync(w.gemm_ws, 0, w.gemm_ws_bytes, st) != cudaSuccess) return QOQ_ERR_CUDA;
     if (M > kFuseMaxM || !fused) {
         if ((rc = qoq_quantize_activations_per_token(X, M, K, ldx, w.qx, w.sx, w.tx, st))) return rc;
         return run_gemm(w.qx, w.sx, w.tx, packed, s0, M, N, K, group, Y, ldy, false, w.gemm_ws, w.gemm_ws_bytes,
@@ -344,6 +349,174 @@ int qoq_linear_host(const void* X_host, int M, int K, const void* packed, const 
     if (cudaMemcpyAsync(Y_host, Yd, (size_t)M * N * 2, cudaMemcpyDeviceToHost, st) != cudaSuccess)
         return QOQ_ERR_CUDA;
     return QOQ_OK;
+}
+
+}  // extern "C"
+
+// ---- decode chain (w4a8_chain.cu)
+
+namespace {
+
+struct ChainWs {
+    int* exitcnt;
+    int* qdone;
+    int* done;
+    int* tilecnt[2];
+    int32_t* slots[2];
+    int8_t* qx[2];
+    int4* meta[2];
+    int ldq;
+    size_t total;
+};
+
+// [exitcnt 256 B][qdone 256 x 4][done 256 x 4][tilecnt x2 [512][2]] (a FIXED head of kChainCounterBytes:
+// the only part that must be zero, left zero by every call, so one workspace serves any chain) |
+// partial slots x2 [2 G][BN][128] i32 | q_x x2 [M][ldq] | meta x2 [M][16 B], 256-B aligned parts.
+ChainWs chain_ws_layout(void* base, int M, int n, const qoq_linear_desc* d, int sms) {
+    ChainWs w{};
+    int kmax = 128;
+    for (int j = 0; j < n; ++j) kmax = d[j].K > kmax ? d[j].K : kmax;
+    const int BN = chain_bn(M);
+    w.ldq = kmax;
+    uint8_t* b = static_cast<uint8_t*>(base);
+    w.exitcnt = reinterpret_cast<int*>(b);
+    w.qdone = reinterpret_cast<int*>(b + 256);
+    w.done = reinterpret_cast<int*>(b + 256 + 4 * kChainMaxJobs);
+    for (int i = 0; i < 2; ++i)
+        w.tilecnt[i] = reinterpret_cast<int*>(b + 256 + 8 * kChainMaxJobs + (size_t)i * kChainMaxNT * 8);
+    size_t off = kChainCounterBytes;
+    for (int i = 0; i < 2; ++i) { w.slots[i] = reinterpret_cast<int32_t*>(b + off); off += (size_t)2 * sms * BN * 128 * 4; }
+    for (int i = 0; i < 2; ++i) { w.qx[i] = reinterpret_cast<int8_t*>(b + off); off += align_up((size_t)M * kmax, 256); }
+    for (int i = 0; i < 2; ++i) { w.meta[i] = reinterpret_cast<int4*>(b + off); off += align_up((size_t)M * 16, 256); }
+    w.total = off;
+    return w;
+}
+
+int chain_desc_status(int M, int n, const qoq_linear_desc* d) {
+    if (M < 1 || M > kChainMaxM || n < 1 || n > kChainMaxJobs || !d) return QOQ_ERR_INVALID_ARG;
+    for (int j = 0; j < n; ++j) {
+        int rc = gemm_shape_status(M, d[j].N, d[j].K, 128);
+        if (rc) return rc;
+        if (d[j].N > kChainMaxNT * kTileN || d[j].K > kChainQMaxK) return QOQ_ERR_SHAPE;
+        if (d[j].ldx < d[j].K || d[j].ldx % 8 || d[j].ldy < d[j].N || d[j].ldy % 8) return QOQ_ERR_INVALID_ARG;
+        if (!d[j].X_fp16 || !d[j].packed || !d[j].s0_fp16 || !d[j].Y_fp16) return QOQ_ERR_INVALID_ARG;
+        if (!aligned16(d[j].X_fp16) || !aligned16(d[j].packed) || !aligned16(d[j].s0_fp16) || !aligned16(d[j].Y_fp16))
+            return QOQ_ERR_INVALID_ARG;
+    }
+    return QOQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t qoq_linear_chain_workspace_bytes(int M, int n, const qoq_linear_desc* desc) {
+    if (chain_desc_status(M, n, desc) != QOQ_OK) return 0;
+    return chain_ws_layout(nullptr, M, n, desc, num_sms_or_default()).total;
+}
+
+static int run_chain(int M, int n, const qoq_linear_desc* desc, void* workspace, size_t workspace_bytes,
+                     void* stream, void* trace) {
+    int rc = chain_desc_status(M, n, desc);
+    if (rc) return rc;
+    if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return QOQ_ERR_INVALID_ARG;
+    ChainWs w = chain_ws_layout(workspace, M, n, desc, num_sms_or_default());
+    if (workspace_bytes < w.total) return QOQ_ERR_WORKSPACE;
+    int sms = 0;
+    if ((rc = check_arch(&sms))) return rc;
+    if (sms != num_sms_or_default()) return QOQ_ERR_CUDA;
+    std::unique_ptr<ChainParams> pp(new ChainParams());   // ~16 KB of launch parameters (host heap)
+    const char* sc = getenv("QOQ_CHAIN_SMAX");              // tuning: cap on the k-splits per tile
+    const int chain_s_cap = sc ? atoi(sc) : 0;
+    ChainParams& p = *pp;
+    p.M = M;
+    p.njobs = n;
+    p.G = sms;
+    for (int i = 0; i < 2; ++i) {
+        p.qx[i] = w.qx[i];
+        p.meta[i] = w.meta[i];
+        p.slots[i] = w.slots[i];
+        p.tilecnt[i] = w.tilecnt[i];
+    }
+    p.ldq = w.ldq;
+    auto enc = tensor_map_encoder();
+    if (!enc) return QOQ_ERR_CUDA;
+    int map_par[kChainMaxMaps], map_k[kChainMaxMaps];
+    p.nmaps = 0;
+    p.qdone = w.qdone;
+    p.done = w.done;
+    p.exitcnt = w.exitcnt;
+    p.trace = static_cast<unsigned long long*>(trace);
+    for (int j = 0; j < n; ++j) {
+        ChainJob& J = p.job[j];
+        J.packed = static_cast<const uint8_t*>(desc[j].packed);
+        J.s0 = static_cast<const __half*>(desc[j].s0_fp16);
+        J.X = static_cast<const __half*>(desc[j].X_fp16);
+        J.Y = static_cast<__half*>(desc[j].Y_fp16);
+        J.ldx = desc[j].ldx;
+        J.ldy = desc[j].ldy;
+        J.K = desc[j].K;
+        J.KT = desc[j].K / kTileK;
+        J.KS = (J.KT + 1) / 2;
+        J.NT = desc[j].N / kTileN;
+        J.I = (long long)J.NT * J.KS;
+        // the TMA map of this linear's q_x: (parity, K) -> dims {K, M}, box {128, BN}, SWIZZLE_128B
+        J.tm = -1;
+        for (int i = 0; i < p.nmaps; ++i)
+            if (map_par[i] == (j & 1) && map_k[i] == J.K) J.tm = i;
+        if (J.tm < 0) {
+            if (p.nmaps == kChainMaxMaps) return QOQ_ERR_UNSUPPORTED;
+            const int i = p.nmaps++;
+            map_par[i] = j & 1;
+            map_k[i] = J.K;
+            cuuint64_t dims[2] = {(cuuint64_t)J.K, (cuuint64_t)M};
+            cuuint64_t strides[1] = {(cuuint64_t)w.ldq};
+            cuuint32_t box[2] = {128u, (cuuint32_t)chain_bn(M)};
+            cuuint32_t estr[2] = {1u, 1u};
+            if (enc(&p.tmap[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, w.qx[j & 1], dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return QOQ_ERR_CUDA;
+            J.tm = i;
+        }
+        // decode-sized linears (fewer tiles than SMs): S equal k-splits per tile, one segment per CTA;
+        // otherwise stream-K over all CTAs (no wave quantization)
+        // (at most 4 splits: a finalizer stages every contributor's 32-row block of its slice in 32 KB)
+        J.S = J.NT < sms ? std::min(std::min(sms / J.NT, J.KS), 4) : 0;
+        if (J.S > 0 && chain_s_cap > 0) J.S = std::min(J.S, chain_s_cap);
+        {   // the TMA map of Y_j: dims {N, M} fp16, row stride ldy, box {32, min(BN, 64)}
+            cuuint64_t dims[2] = {(cuuint64_t)desc[j].N, (cuuint64_t)M};
+            cuuint64_t strides[1] = {(cuuint64_t)desc[j].ldy * 2};
+            cuuint32_t box[2] = {32u, (cuuint32_t)std::min(chain_bn(M), 64)};
+            cuuint32_t estr[2] = {1u, 1u};
+            if (enc(&p.ymap[j], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, desc[j].Y_fp16, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return QOQ_ERR_CUDA;
+        }
+        if (J.S > 0) {
+            J.units = J.NT * J.S;
+        } else {   // (CTA, segment) pairs of the stream-K split
+            long long units = 0;
+            for (int b = 0; b < sms; ++b) {
+                const long long c0 = (long long)b * J.I / sms, c1 = (long long)(b + 1) * J.I / sms;
+                if (c1 > c0) units += (c1 - 1) / J.KS - c0 / J.KS + 1;
+            }
+            J.units = (int)units;
+        }
+    }
+    return launch_w4a8_chain(p, static_cast<cudaStream_t>(stream)) == cudaSuccess ? QOQ_OK : QOQ_ERR_CUDA;
+}
+
+int qoq_w4a8_linear_chain(int M, int n, const qoq_linear_desc* desc, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+    return run_chain(M, n, desc, workspace, workspace_bytes, stream, nullptr);
+}
+
+// Debug (not in the public header): the chain with a [n][G][8] u64 %globaltimer trace (trace builds).
+int qoq_debug_w4a8_linear_chain_trace(int M, int n, const qoq_linear_desc* desc, void* workspace,
+                                      size_t workspace_bytes, void* trace, void* stream) {
+    return run_chain(M, n, desc, workspace, workspace_bytes, stream, trace);
 }
 
 }  // extern "C"

@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
 #include <cstddef>
 #include <cstdint>
 
@@ -55,6 +57,8 @@ struct GemmArgs {
 constexpr int kFuseMaxM = 64;   // above: quantizer kernel + GEMM (the prologue would serialize M rows)
 
 cudaError_t launch_w4a8_gemm(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (nullptr if unavailable)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 cudaError_t launch_quantize_weights(const void* W, int N, int K, void* packed, void* s0, cudaStream_t st);
 cudaError_t launch_pc_quantize_weights(const void* W, int N, int K, void* packed, void* s_w, uint8_t* z_w,
                                        cudaStream_t st);
@@ -73,5 +77,42 @@ cudaError_t launch_kv4_append(const void* K, const void* V, const int32_t* slots
 cudaError_t launch_kv4_decode_attention(const void* Q, const uint8_t* pages, const int32_t* block_table,
                                         const int32_t* seq_lens, int B, int H, int H_kv, int P, int max_pages,
                                         void* O, cudaStream_t st);
+
+// Persistent decode chain (w4a8_chain.cu): n W4A8 linear layers in one launch, M <= 128.
+constexpr int kChainMaxJobs = 128;    // (one 128-byte Y tensor map per linear in the ~28 KB of parameters)
+constexpr int kChainMaxM = 128;
+constexpr int kChainMaxNT = 512;        // N <= 65536 per linear
+constexpr int kChainQMaxK = 14336;      // K per linear (the in-kernel quantizer stages one row in SMEM)
+constexpr int kChainCounterBytes = 12288;   // fixed-size zero-required head of the chain workspace
+constexpr int kChainMaxMaps = 16;      // distinct (parity, K) activation tensor maps per chain
+struct ChainJob {            // one linear layer (host-planned)
+    const uint8_t* packed;   // tile stream [NT][KT][8448]
+    const __half* s0;        // [N]
+    const __half* X;         // input [M][ldx] fp16 (may be an earlier job's Y)
+    __half* Y;               // output [M][ldy] fp16 (ldy % 8 == 0: 16-byte TMA store runs)
+    int ldx, ldy, K, KT, KS, NT;
+    int S;                   // k-splits per tile (NT < G: CTA b -> tile b / S), 0 = stream-K over all CTAs
+    int units;               // (CTA, segment) pairs: the job is complete when done[j] reaches it
+    int tm;                  // index of the TMA map of its q_x (parity j & 1, this K)
+    long long I;             // NT * KS pipeline steps
+};
+struct ChainParams {
+    CUtensorMap ymap[kChainMaxJobs];   // Y_j maps: dims {N, M} fp16, row stride ldy, box {32, min(BN, 64)}
+    CUtensorMap tmap[kChainMaxMaps];   // q_x maps: dims {K, M}, row stride ldq, box {128, BN}, SWIZZLE_128B
+    int M, njobs, G, nmaps;  // tokens, linears, CTAs (one per SM), maps
+    int ldq;                 // q_x row stride (bytes)
+    int8_t* qx[2];           // q_x [M][ldq] int8 (job parity)
+    int4* meta[2];           // [M] {s_x fp16 bits, t_x, 0, 0}
+    int32_t* slots[2];       // split-K partial tiles, one slot per (CTA, first/last segment): [2G][BN][128] int32
+    int* tilecnt[2];         // per tile: partials landed, slices finalized [kChainMaxNT][2] (zero between uses)
+    int* qdone;              // [njobs] rows quantized (zero at launch, re-zeroed at exit)
+    int* done;               // [njobs] units complete
+    int* exitcnt;            // CTAs finished
+    unsigned long long* trace;   // debug (QOQ_TRACING builds): [njobs][G][32] stamps x2, else null
+    ChainJob job[kChainMaxJobs];
+};
+int chain_bn(int M);
+int chain_block_threads(int M);
+cudaError_t launch_w4a8_chain(const ChainParams& p, cudaStream_t st);
 
 }  // namespace qoq

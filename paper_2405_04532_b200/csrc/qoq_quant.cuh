@@ -120,4 +120,41 @@ __device__ __forceinline__ uint2 quant8(uint4 u, float s, float inv, int& t) {
     return make_uint2(w[0], w[1]);
 }
 
+// quant8 with the exact division only for the element(s) near a tie (the persistent chain's quantizer,
+// where one slow row delays the whole grid): bit-identical to quant8.
+__device__ __forceinline__ uint2 quant8_pe(uint4 u, float s, float inv, int& t) {
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+    float x[8], r[8];
+    bool near_tie = false;
+    uint32_t near = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(h[e]);
+        x[2 * e] = f.x;
+        x[2 * e + 1] = f.y;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float rc = fminf(fmaxf(__fmul_rn(x[i], inv), -127.0f), 127.0f);
+        const float ri = rintf(rc);
+        const bool nt = fabsf(rc - ri) >= 0.5f - 0x1p-14f;
+        near |= (uint32_t)nt << i;
+        near_tie |= nt;
+        r[i] = ri;
+    }
+    if (near_tie) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (near & (1u << i)) r[i] = (float)quant_code_exact(x[i], s);
+    }
+    uint32_t w[2] = {0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int q = __float2int_rz(r[i]);   // r[i] is integer-valued
+        t += q;
+        w[i >> 2] |= (uint32_t)(q & 0xff) << (8 * (i & 3));
+    }
+    return make_uint2(w[0], w[1]);
+}
+
 }  // namespace qoq

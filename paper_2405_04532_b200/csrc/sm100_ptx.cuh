@@ -47,10 +47,18 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
     return ok != 0;
 }
 
+// QOQ_WATCHDOG=1 (debug builds only, e.g. `build.py --variant=wd:-DQOQ_WATCHDOG=1`): every mbarrier
+// wait and flag spin traps after ~2^26 polls, turning a pipeline deadlock into a kernel error instead of
+// a hung GPU. Off in production: a legitimate wait can exceed any fixed poll count under
+// compute-sanitizer, preemption or MPS time slicing.
+#ifndef QOQ_WATCHDOG
+#define QOQ_WATCHDOG 0
+#endif
+
 // Wait until the phase with the given parity has completed: one PTX loop (no C-level loop, so no
-// convergence barriers or YIELDs around it). A watchdog turns a pipeline deadlock into a kernel trap
-// (an error the caller sees) instead of a hung GPU.
+// convergence barriers or YIELDs around it).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if QOQ_WATCHDOG
     asm volatile(
         "{\n\t.reg .pred p;\n\t.reg .u32 c;\n\t"
         "mov.u32 c, 0;\n"
@@ -64,6 +72,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "QOQ_DONE_%=:\n\t}"
         ::"r"(smem_u32(bar)), "r"(parity)
         : "memory");
+#else
+    // suspend-time hint (ns): a waiting warp is parked until the phase completes (or the hint runs
+    // out) instead of re-issuing try_wait, leaving the issue slots to the working warps
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "QOQ_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra.uni QOQ_WAIT_%=;\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+#endif
 }
 
 // One elected lane of a fully active warp (elect.sync).
@@ -95,9 +114,22 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, in
         : "memory");
 }
 
+// 2-D tensor-map store shared -> global (box defined by the tensor map; out-of-bounds parts clipped).
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                 ::"l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(smem_src))
+                 : "memory");
+}
+
 // Bulk reduce-add of `bytes` of int32 from shared to global, performed in L2 (bulk_group).
 __device__ __forceinline__ void bulk_reduce_add_s32(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.s32 [%0], [%1], %2;"
+                 ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+// Bulk copy of `bytes` from shared to global memory (bulk_group completion).
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                  ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
                  : "memory");
 }
@@ -131,8 +163,8 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
     return r;
 }
-// gpu-scope acquire load / bounded spin (the fused quantization's grid handshake). The spin traps
-// after ~2^26 polls instead of hanging the device if an arrival never comes.
+// gpu-scope acquire load / spin (grid handshakes); the spin traps after ~2^26 polls in QOQ_WATCHDOG
+// builds only.
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -142,8 +174,26 @@ __device__ __forceinline__ void red_release_add_gpu(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void spin_until_ge(const int* p, int target) {
+#if QOQ_WATCHDOG
     for (uint32_t n = 0; ld_acquire_gpu(p) < target; ++n)
         if (n == (1u << 26)) __trap();
+#else
+    while (ld_acquire_gpu(p) < target) {
+    }
+#endif
+}
+
+// Spin with a short back-off between polls: many CTAs polling one L2 line otherwise queue the very
+// release (red) they are waiting for behind their loads.
+__device__ __forceinline__ void spin_until_ge_backoff(const int* p, int target) {
+#if QOQ_WATCHDOG
+    for (uint32_t n = 0; ld_acquire_gpu(p) < target; ++n) {
+        if (n == (1u << 24)) __trap();
+        __nanosleep(64);
+    }
+#else
+    while (ld_acquire_gpu(p) < target) __nanosleep(64);
+#endif
 }
 
 // 32-bit loads / stores to (possibly remote) cluster shared memory (address from mapa_shared)

@@ -31,32 +31,13 @@
 #include "qoq_internal.h"
 #include "sm100_ptx.cuh"
 #include "qoq_quant.cuh"
-
-// Timing ablations (never in production builds; results are garbage when set):
-//   2: no activation TMA (xfull arrives without data)   4: no weight bulk copies (wfull arrives)
-//   8: dequant skips the ALU expansion   16: dequant skips the TMEM stores
-#ifndef QOQ_ABLATE
-#define QOQ_ABLATE 0
-#endif
+#include "w4a8_common.cuh"
 
 namespace qoq {
 
 #ifndef QOQ_DEQ_GROUPS
 #define QOQ_DEQ_GROUPS 3
 #endif
-
-// Warp roles (per Cfg): 0 weight producer, 1 MMA issuer 0 + TMEM owner, 2 .. 2+4G-1 dequant (G groups
-// of 4 warps taking steps round-robin), then 4 epilogue warps, MMA issuer 1, activation producer.
-template <int G>
-struct Roles {
-    static constexpr int kDeqGroups = G;
-    static constexpr int kDeqWarp1 = 2 + 4 * G;          // first warp after the dequant warps
-    static constexpr int kEpiWarp0 = kDeqWarp1;          // epilogue: 4 warps
-    static constexpr int kMma1Warp = kEpiWarp0 + 4;      // MMA issuer 1
-    static constexpr int kXProdWarp = kMma1Warp + 1;     // activation producer
-    static constexpr int kBlockThreads = 32 * (kXProdWarp + 1);
-    static constexpr int kEpiThread0 = 32 * kEpiWarp0;   // first epilogue thread
-};
 
 // One pipeline STEP = up to two consecutive 128-deep k-tiles of one output tile: the handoff
 // (dequant -> MMA, MMA -> producer) is amortized over 8 MMAs, and two MMA-issuing warps take
@@ -121,14 +102,20 @@ struct Cfg {
     static constexpr int kARaw0 = (512 - kAccCols) / 64;
     static constexpr int kARaw = kARaw0 > 6 ? 6 : kARaw0;
     static constexpr int kAStages = (kARaw / kARot) * kARot;
-    static constexpr int kXStagesDef = BN <= 32 ? (kDeqGroups == 3 ? 6 : 8) : BN == 64 ? 6 : 2;
+#ifndef QOQ_XSTAGES64
+#define QOQ_XSTAGES64 6
+#endif
+#ifndef QOQ_SMEM_KB
+#define QOQ_SMEM_KB 212
+#endif
+    static constexpr int kXStagesDef = BN <= 32 ? (kDeqGroups == 3 ? 6 : 8) : BN == 64 ? QOQ_XSTAGES64 : 2;
 #ifndef QOQ_XSTAGES
     static constexpr int kXStages = kXStagesDef;
 #else
     static constexpr int kXStages = (BN <= 64 && CG == 1) ? QOQ_XSTAGES : kXStagesDef;
 #endif
     static constexpr int kWStageBytes = ((2 * kTB + 1023) / 1024) * 1024;   // packed weights of one step
-    static constexpr int kWRaw = (212 * 1024 - kEpiBytes - kXStages * kXStageBytes) / kWStageBytes;
+    static constexpr int kWRaw = (QOQ_SMEM_KB * 1024 - kEpiBytes - kXStages * kXStageBytes) / kWStageBytes;
     static constexpr int kWCap = kWRaw > 12 ? 12 : kWRaw;
     static constexpr int kWStages = (kWCap / kDeqRot) * kDeqRot;
     static constexpr int kColsUsed = kAStages * 64 + kAccCols;
@@ -335,28 +322,6 @@ __device__ __forceinline__ void write_out4(const KParams& p, int m, int n, int4 
     }
 }
 
-// Expand one 128-weight row of a packed tile (4 x 16 B = 128 u4 codes) into 32 TMEM words of
-// four 8-bit lanes each: lane = q_u4 * s_u8 + (128 - z*s_u8) = q̂ + 128 ∈ [7, 254] (no cross-lane
-// carry: the protective range bounds q̂ to [-121, 126]). SIGNED additionally flips the
-// lane MSBs (XOR 0x80) to give q̂ as s8. Per 8 weights: 2 LOP3 (ALU pipe) + IMAD.HI (the >> 4, on
-// the FMA pipe) + 2 IMAD (FMA pipe) [+ 2 LOP3], balancing the two integer pipes.
-template <bool SIGNED>
-__device__ __forceinline__ void expand_row(const uint4 (&v)[4], uint32_t s, uint32_t bias, uint32_t (&out)[32]) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const uint32_t wd[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t lo = wd[i] & 0x0F0F0F0Fu;                      // k = 32c + 4i .. +3
-            const uint32_t hi = __umulhi(wd[i], 0x10000000u) & 0x0F0F0F0Fu;   // (w >> 4): k = 32c + 16 + 4i ..
-            uint32_t a = lo * s + bias, b = hi * s + bias;
-            if (SIGNED) { a ^= 0x80808080u; b ^= 0x80808080u; }
-            out[c * 8 + i] = (QOQ_ABLATE & 8) ? wd[i] : a;
-            out[c * 8 + 4 + i] = (QOQ_ABLATE & 8) ? wd[i] : b;
-        }
-    }
-}
-
 // Fused per-token quantization by the 128 epilogue threads (et) of this CTA: rows m ≡ blockIdx.x
 // (mod gridDim.x), same arithmetic as quantize_act_kernel (qoq_quant.cuh): amax with kQVec loads
 // per thread in flight, then a compact quantize loop over the (L1-resident) row. red/redi: >= 4
@@ -435,22 +400,7 @@ __device__ __forceinline__ void fused_depart(const KParams& p) {
 
 template <int BN>
 __device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<BN, 1>::kChunk]) {
-    if constexpr (Cfg<BN>::kChunk == 32) tmem_ld_32x32b_x32(taddr, v);
-    else tmem_ld_32x32b_x16(taddr, v);
-}
-
-// Zero this warp's 32 TMEM lanes of a BN-column accumulator (tcgen05.st, then wait::st).
-template <int BN>
-__device__ __forceinline__ void zero_acc(uint32_t taddr) {
-    if constexpr (BN >= 32) {
-        const uint32_t z[32] = {0};
-#pragma unroll
-        for (int c = 0; c < BN; c += 32) tmem_st_32x32b_x32(taddr + c, z);
-    } else {
-        const uint32_t z[16] = {0};
-        tmem_st_32x32b_x16(taddr, z);
-    }
-    tmem_wait_st();
+    tmem_ld_cols<Cfg<BN, 1>::kChunk>(taddr, v);
 }
 
 template <int BN, bool OUT_I32, int CG, bool PC = false>
@@ -1016,7 +966,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC>::kBlockThreads, 1)
 
 // ------------------------------------------------------------------ host side
 
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;   // resolved once; immutable after
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -1173,7 +1123,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     auto kern = w4a8_gemm_kernel<BN, OUT_I32, CG, PC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    auto enc = encode_fn();
+    auto enc = tensor_map_encoder();
     if (!enc) return cudaErrorNotSupported;
     CUtensorMap tm;
     cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.M};

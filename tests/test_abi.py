@@ -45,7 +45,7 @@ def test_library_is_sm100a_only(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert lib.qoq_abi_version() == 5
+    assert lib.qoq_abi_version() == 6
     for s in range(0, 8):
         assert lib.qoq_status_string(s)
 
@@ -148,3 +148,38 @@ def test_kv4_validation(lib):
     assert lib.qoq_kv4_decode_attention(fake, fake, fake, fake, 4, 32, 8, 128, 64, 0, fake, None) == 1
     assert lib.qoq_kv4_decode_attention(P((1 << 20) + 8), *args[1:]) == 1
     assert lib.qoq_kv4_decode_attention(fake, fake, fake, fake, 0, 32, 8, 128, 64, 16, fake, None) == 0
+
+
+def test_linear_chain_validation(lib):
+    """qoq_w4a8_linear_chain / qoq_linear_chain_workspace_bytes (ABI v6): host-side validation of the
+    descriptor array, M and n ranges and the workspace size — all before any device call."""
+    import paper_2405_04532_b200 as qoq
+    P, Z = ctypes.c_void_p, ctypes.c_size_t
+    lib.qoq_linear_chain_workspace_bytes.restype = Z
+    lib.qoq_linear_chain_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_int, P]
+    lib.qoq_w4a8_linear_chain.restype = ctypes.c_int
+    lib.qoq_w4a8_linear_chain.argtypes = [ctypes.c_int, ctypes.c_int, P, P, Z, P]
+    fake = 1 << 20
+    D = qoq.LinearDesc
+    good = (D * 2)(D(fake, 4096, 6144, 4096, fake, fake, fake, 6144), D(fake, 6144, 4096, 6144, fake, fake, fake, 4096))
+    nb = lib.qoq_linear_chain_workspace_bytes(64, 2, good)
+    # counters + 2 x split-K partial tiles [NT max = 48][BN = 64][128] i32 + 2 x q_x [KT max = 48][64][128]
+    assert nb >= 2 * 48 * 64 * 128 * 4 + 2 * 48 * 64 * 128
+    assert lib.qoq_linear_chain_workspace_bytes(0, 2, good) == 0        # M out of range
+    assert lib.qoq_linear_chain_workspace_bytes(129, 2, good) == 0
+    assert lib.qoq_linear_chain_workspace_bytes(64, 0, good) == 0       # n out of range
+    assert lib.qoq_w4a8_linear_chain(64, 2, good, None, Z(nb), None) == 1            # no workspace
+    assert lib.qoq_w4a8_linear_chain(64, 2, good, P(fake), Z(nb - 256), None) == 5   # too small
+    assert lib.qoq_w4a8_linear_chain(64, 129, good, P(fake), Z(nb), None) == 1       # n > 128
+    big_k = (D * 1)(D(fake, 16384, 128, 16384, fake, fake, fake, 128))          # K > 14336 (quantizer staging)
+    assert lib.qoq_w4a8_linear_chain(64, 1, big_k, P(fake), Z(1 << 30), None) == 2
+    bad_ldy = (D * 1)(D(fake, 4096, 128, 4096, fake, fake, fake, 132))         # ldy % 8 != 0
+    assert lib.qoq_w4a8_linear_chain(64, 1, bad_ldy, P(fake), Z(1 << 30), None) == 1
+    bad_shape = (D * 1)(D(fake, 4096, 100, 4096, fake, fake, fake, 128))
+    assert lib.qoq_w4a8_linear_chain(64, 1, bad_shape, P(fake), Z(1 << 30), None) == 2
+    bad_ld = (D * 1)(D(fake, 4000, 128, 4096, fake, fake, fake, 128))            # ldx < K
+    assert lib.qoq_w4a8_linear_chain(64, 1, bad_ld, P(fake), Z(1 << 30), None) == 1
+    bad_al = (D * 1)(D(fake + 8, 4096, 128, 4096, fake, fake, fake, 128))        # X misaligned
+    assert lib.qoq_w4a8_linear_chain(64, 1, bad_al, P(fake), Z(1 << 30), None) == 1
+    null_y = (D * 1)(D(fake, 4096, 128, 4096, fake, fake, None, 128))
+    assert lib.qoq_w4a8_linear_chain(64, 1, null_y, P(fake), Z(1 << 30), None) == 1
