@@ -99,23 +99,12 @@ def model_shapes(model, fused=True):
 
 
 def layer_shapes(model, M, world, rank, fused=True):
-    """Per-rank GEMM list of one layer: (name, N_r, K_r, kind, quant_group). Column-parallel layers
-    split N (a fused gate_up shard holds the rank's gate rows and up rows), row-parallel layers split
-    K (both at 128 boundaries). quant_group names which activation quantization feeds the GEMM
-    (gate and up share one, as in Fig. 7)."""
-    shapes = model_shapes(model, fused)
-    out = []
-    for name, N, K, kind in shapes:
-        if kind == "col":
-            assert N % (128 * world) == 0
-            Nr, Kr = N // world, K
-        else:
-            assert K % (128 * world) == 0
-            Nr, Kr = N, K // world
-        qg = {"qkv": "attn_in", "o": "attn_out", "gate": "mlp_in", "up": "mlp_in", "gate_up": "mlp_in",
-              "down": "mlp_act"}[name]
-        out.append((name, Nr, Kr, kind, qg))
-    return out
+    """Per-rank GEMM list of one layer: [(name, N_r, K_r, kind, quant_group)] (parallel.rank_layer_plan:
+    column-parallel layers split N, a fused gate_up shard holds the rank's gate rows and up rows,
+    row-parallel layers split K, both at 128 boundaries)."""
+    from paper_2405_04532_b200 import parallel
+    return [(name, Nr, Kr, kind, qg) for name, Nr, Kr, N, K, kind, qg in
+            parallel.rank_layer_plan(model_shapes(model, fused), world)]
 
 
 def step_work(model, M, layers, world, fused=True):
@@ -188,15 +177,30 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ reference arm / cpu baseline (the oracle)
 
-def oracle_sample(seconds_min=10.0, reps_max=200, M=64):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def oracle_sample(seconds_min=10.0, reps_max=200, M=64, threads=0):
     """The CPU oracle, as it stands, on a bounded sample of the workload: layer 0's o_proj
     (4096x4096, g=128) at decode M, full work (O4 quantize -> O3^-1 unpack -> level-2 dequant ->
-    O5 INT32 GEMM -> O6 fp64 epilogue), repeated until >= seconds_min. Returns (GB/s, detail)."""
+    O5 INT32 GEMM -> O6 fp64 epilogue), repeated until >= seconds_min. threads: OpenMP threads of the
+    GEMM loops (0 = all host cores). Returns (GB/s, detail)."""
     import oracle
     N, K = 4096, 4096
     W = synth.weights_fp16(N, K, seed=0)
     X = synth.activations_fp16(M, K, seed=0)
     packed, s0 = oracle.quantize_weights(W)
+    all_threads = os.cpu_count() or 1
+    oracle.set_num_threads(threads if threads > 0 else all_threads)
     t0 = time.perf_counter()
     reps = 0
     while reps < reps_max:
@@ -205,9 +209,20 @@ def oracle_sample(seconds_min=10.0, reps_max=200, M=64):
         if time.perf_counter() - t0 >= seconds_min:
             break
     dt = time.perf_counter() - t0
+    used = oracle.num_threads()
+    oracle.set_num_threads(all_threads)
     b = (gemm_bytes(M, N, K) + quant_bytes(M, K)) * reps
-    return b / dt / 1e9, {"reps": reps, "seconds": dt, "threads": oracle.num_threads(),
+    return b / dt / 1e9, {"reps": reps, "seconds": dt, "threads": used,
                            "sample": f"layer-0 o_proj {N}x{K} g128 at M={M}, quantize+GEMM+epilogue, x{reps}"}
+
+
+def cpu_baseline_line():
+    """The oracle timed on all host cores and on one core (SURVEY §8(d) "Oracle timing"), with the CPU model."""
+    v, d = oracle_sample()
+    v1, d1 = oracle_sample(seconds_min=4.0, threads=1)
+    return {"value": v, "unit": UNIT, "cores": d["threads"], "kind": "oracle", "sample": d["sample"],
+            "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "sample": d1["sample"]},
+            "cpu_model": cpu_model(), "host_cpus": os.cpu_count()}
 
 
 def run_reference(args):
@@ -229,12 +244,16 @@ def run_reference(args):
     b = (gemm_bytes(M, N, K) + quant_bytes(M, K)) * args.steps
     v = b / dt / 1e9
     sample = f"each step: layer-0 o_proj {N}x{K} g128 at M={M} (quantize + W4A8 GEMM + epilogue) on the CPU oracle"
+    cfg = config_dict(args, 1)
+    cfg["workload"] = (f"{args.model} decode linear stack (reference arm: each step is a bounded sample of it, "
+                       f"layer 0's o_proj {N}x{K} at M={M} with its quantizer, on the CPU oracle; GB/s of that "
+                       f"sample's algorithmic bytes)")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "config": config_dict(args, 1),
+            "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -275,6 +294,8 @@ def main():
     ap.add_argument("--no-per-channel", action="store_true",
                     help="skip the per-channel W4A8 (NEXT-1) decode step measurement")
     ap.add_argument("--unfused-gate-up", action="store_true", help="run gate and up as two GEMMs")
+    ap.add_argument("--no-chain", action="store_true", help="skip the persistent decode chain measurement")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the decode M sweep (C2: M = 1 .. 256)")
     ap.add_argument("--fused-quant", action="store_true",
                     help="qoq_w4a8_linear per linear: per-token quantization fused into the GEMM prologue "
                          "(M <= 64); default: quantizer kernel + GEMM, chained with PDL (faster today)")
@@ -295,36 +316,46 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")           # communicator init (transport, NVLS) on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     qoq.load()
+    from paper_2405_04532_b200 import parallel
     M = args.M
     layers = args.layers or synth.MODELS[args.model][1]
     fused = not args.unfused_gate_up
-    shapes = layer_shapes(args.model, M, world, rank, fused)
+    plan = parallel.rank_layer_plan(model_shapes(args.model, fused), world)
+    shapes = [(name, Nr, Kr, kind, qg) for name, Nr, Kr, N, K, kind, qg in plan]
     stream = torch.cuda.Stream(dev)
 
-    # ---- offline: pack every layer's weights on device (row a1), distinct per layer
-    packed = []   # [layer][i] -> (packed, s0)
+    # ---- offline: pack every layer's FULL weights on device (row a1; the same seeded weights on every
+    # rank, distinct per layer), then keep this rank's shards (parallel.shard_layer): the TP ranks hold
+    # exactly the 1-GPU quantized weights
+    packed = []   # [layer][i] -> (packed_r, s0_r)
     gen = torch.Generator(device=dev)
     with torch.cuda.stream(stream):
         for l in range(layers):
-            row = []
-            for i, (name, N, K, kind, qg) in enumerate(shapes):
-                gen.manual_seed(1000 * l + 17 * i + rank)
+            full = []
+            for i, (name, Nr, Kr, N, K, kind, qg) in enumerate(plan):
+                gen.manual_seed(1000 * l + 17 * i)
                 W = synth.device_weights_fp16(N, K, gen, dev)
-                row.append(qoq.quantize_weights(W, stream=stream))
+                full.append(qoq.quantize_weights(W, stream=stream))
                 del W
-            packed.append(row)
+            packed.append([(p.contiguous(), s0.contiguous()) for p, s0 in parallel.shard_layer(full, plan, rank, world)])
+            del full
     stream.synchronize()
 
-    # ---- activations (L2-resident, as when produced by the preceding kernel in a real decode)
+    # ---- activations (L2-resident, as when produced by the preceding kernel in a real decode): one full
+    # [M][K] input per quantization group, replicated on every rank; a row-parallel rank quantizes its
+    # K-shard view (row stride K)
     gen.manual_seed(7)
     Kin = {}
-    for name, N, K, kind, qg in shapes:
+    for name, Nr, Kr, N, K, kind, qg in plan:
         Kin[qg] = K
     X = {qg: synth.device_activations_fp16(M, K, gen, dev) for qg, K in Kin.items()}
+    Kq = {qg: (Kr if kind == "row" else K) for name, Nr, Kr, N, K, kind, qg in plan}
     quant_out = {qg: (torch.empty(M, K, dtype=torch.int8, device=dev), torch.empty(M, dtype=torch.float16, device=dev),
-                      torch.empty(M, dtype=torch.int32, device=dev)) for qg, K in Kin.items()}
+                      torch.empty(M, dtype=torch.int32, device=dev)) for qg, K in Kq.items()}
     Ybuf = {name: torch.empty(M, N, dtype=torch.float16, device=dev) for name, N, K, kind, qg in shapes}
     ws = qoq.Workspace(dev)      # GEMM workspace (kept all-zero by the library)
     ws.get(max(qoq.gemm_workspace_bytes(M, N, K) for _, N, K, _, _ in shapes))
@@ -334,29 +365,35 @@ def main():
     if fused_quant:
         os.environ["QOQ_LINEAR_FUSED"] = "1"   # w4a8_linear's opt-in one-kernel path (read per call)
 
-    def run_step(gemm_only=False):
+    def make_linear(gemm_only, counter):
+        def linear(X_r, shard, entry):
+            name, Nr, Kr, N, K, kind, qg = entry
+            p, s0 = shard
+            if fused_quant and not gemm_only:
+                # the public linear call: per-token quantization fused into the GEMM (M <= 64)
+                Xc = X_r if X_r.is_contiguous() else X_r.contiguous()
+                qoq.w4a8_linear(Xc, p, s0, Nr, out=Ybuf[name], workspace=lws, stream=stream)
+                counter[0] += qoq.linear_launches(M)
+                return Ybuf[name]
+            if not gemm_only and qg not in counter[1]:
+                qoq.quantize_activations_per_token(X_r, out=quant_out[qg], stream=stream)
+                counter[1].add(qg)
+                counter[0] += 1
+            qx, sx, tx = quant_out[qg]
+            qoq.w4a8_gemm(qx, sx, tx, p, s0, Nr, out=Ybuf[name], workspace=ws, stream=stream)
+            counter[0] += 1
+            return Ybuf[name]
+        return linear
+
+    def run_step(gemm_only=False, collective=True):
+        """One decode step: every layer through parallel.tp_decode_layer (the code path the gloo tests
+        drive), the all-reduces of the row-parallel partials on `stream`."""
         n_launch = 0
         for l in range(layers):
-            done = set()
-            for i, (name, N, K, kind, qg) in enumerate(shapes):
-                if fused_quant and not gemm_only:
-                    # the public linear call: per-token quantization fused into the GEMM (M <= 64)
-                    p, s0 = packed[l][i]
-                    qoq.w4a8_linear(X[qg], p, s0, N, out=Ybuf[name], workspace=lws, stream=stream)
-                    n_launch += qoq.linear_launches(M)
-                    if kind == "row" and world > 1:
-                        dist.all_reduce(Ybuf[name])
-                    continue
-                if not gemm_only and qg not in done:
-                    qoq.quantize_activations_per_token(X[qg], out=quant_out[qg], stream=stream)
-                    done.add(qg)
-                    n_launch += 1
-                qx, sx, tx = quant_out[qg]
-                p, s0 = packed[l][i]
-                qoq.w4a8_gemm(qx, sx, tx, p, s0, N, out=Ybuf[name], workspace=ws, stream=stream)
-                n_launch += 1
-                if kind == "row" and world > 1 and not gemm_only:
-                    dist.all_reduce(Ybuf[name])
+            counter = [0, set()]
+            ar = (lambda Y: dist.all_reduce(Y)) if (world > 1 and collective and not gemm_only) else (lambda Y: None)
+            parallel.tp_decode_layer(X, packed[l], plan, make_linear(gemm_only, counter), ar, rank, world)
+            n_launch += counter[0]
         return n_launch
 
     # ---- capture one step as a CUDA graph (launch gaps removed; PDL edges kept)
@@ -370,6 +407,11 @@ def main():
     g_gemm = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g_gemm, stream=stream):
         gemm_launches = run_step(gemm_only=True)
+    g_nocoll = None
+    if world > 1:
+        g_nocoll = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_nocoll, stream=stream):
+            run_step(collective=False)
 
     def timed(graph, steps, warmup):
         for _ in range(warmup):
@@ -399,14 +441,15 @@ def main():
         with sampler:
             ms_total = timed(g_step, args.steps, 0)
         ms_gemm = timed(g_gemm, max(10, args.steps // 2), 2)
+        ms_nocoll = timed(g_nocoll, max(10, args.steps // 2), 2) / max(10, args.steps // 2) if g_nocoll else None
 
     ms_step = ms_total / args.steps
     step_bytes, step_ops = step_work(args.model, M, layers, world, fused)
     value = step_bytes / (ms_step * 1e-3) / 1e9
 
-    # dominant kernel: the W4A8 GEMM. Fused (default, M <= 64): every launch of the step is the GEMM
-    # kernel with the quantization in its prologue, so its per-launch figures come from the step;
-    # two-kernel: the GEMM-only graph.
+    # dominant kernel: the W4A8 GEMM. Fused (M <= 64): every launch of the step is the GEMM kernel with
+    # the quantization in its prologue, so its per-launch figures come from the step; two-kernel: the
+    # GEMM-only graph.
     if fused_quant and qoq.linear_launches(M) == 1:
         rank_gemm_bytes = sum(gemm_bytes(M, N, K) + quant_bytes(M, K) for _, N, K, _, _ in shapes) * layers
         per_launch_ms = ms_step / launches_per_step
@@ -434,6 +477,21 @@ def main():
             "config": config_dict(args, world), "gpu_launches": launches_per_step * args.steps,
             "clocks": sampler.summary(), "roofline": roofline,
             "decode_tops": tops, "decode_frac_int8_datasheet": tops / INT8_DATASHEET_TOPS}
+    if world > 1:
+        # eta_TP = T_roofline,1GPU(full step) / (TP x T_measured,rank), with and without the
+        # all-reduces of the row-parallel partials
+        t_roof = step_bytes / (peak * 1e9) * 1e3
+        line["tp"] = {"world": world, "ms_per_step": ms_step, "ms_per_step_no_collective": ms_nocoll,
+                      "ms_gemm_only": ms_gemm / max(10, args.steps // 2),
+                      "eta_with_collective": t_roof / (world * ms_step),
+                      "eta_no_collective": t_roof / (world * ms_nocoll) if ms_nocoll else None,
+                      "t_roofline_1gpu_ms": t_roof,
+                      "collective": "torch.distributed.all_reduce (NCCL) of the fp16 row-parallel partials"}
+
+    if world == 1 and not args.no_chain and M <= 128:
+        line["decode_chain"] = chain_measure(qoq, torch, args, plan, packed, layers, dev, stream, X, step_bytes, timed)
+    if world == 1 and not args.no_sweep:
+        line["decode_sweep"] = sweep_measure(qoq, torch, args, plan, packed, layers, dev, stream, timed)
 
     # ---- per-channel W4A8 (NEXT-1, §5.2.2): the same decode step on per-channel packed weights
     if not args.no_per_channel and world == 1:
@@ -458,14 +516,21 @@ def main():
 
     if not args.no_prefill:
         line["prefill"] = prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream)
+        if world == 1:
+            # the >= 1024 side of the north_star target (C3 at 4096 / 8192 plus 1024 / 2048)
+            sweep = {}
+            for Mp in (1024, 2048, 4096, 8192):
+                r = prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream, M=Mp, with_ceiling=False)
+                sweep[str(Mp)] = {k: r[k] for k in ("tops", "ms", "frac_int8_datasheet", "per_gemm_tops")}
+                sweep[str(Mp)]["frac_int8_measured_ceiling"] = (r["tops"] / line["prefill"]["int8_ceiling_tops"]
+                                                                 if line["prefill"]["int8_ceiling_tops"] else None)
+            line["prefill"]["sweep"] = sweep
 
     if args.detail:
         line["detail"] = detail_measure(qoq, torch, args, shapes, packed, layers, dev, stream, X)
 
     if rank == 0 and not args.no_cpu_baseline:
-        v, d = oracle_sample()
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": d["threads"], "kind": "oracle",
-                                "sample": d["sample"]}
+        line["cpu_baseline"] = cpu_baseline_line()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -550,6 +615,77 @@ def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stre
             "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": steps, "streams": nstreams,
             "api": "qoq_linear_host (C ABI, pinned host X/Y) per GEMM, calls alternating over "
                    f"{nstreams} streams, the step captured as one CUDA graph"}
+
+
+def chain_measure(qoq, torch, args, plan, packed, layers, dev, stream, X, step_bytes, timed):
+    """The same decode step through the persistent decode chain (qoq_w4a8_linear_chain): every linear of
+    the stack in ONE launch per <= 128 linears, the per-token quantization inside the kernel, each linear
+    waiting for the previous one's output (the sequential dependency of a real decode)."""
+    M = args.M
+    Y = {name: torch.empty(M, N, dtype=torch.float16, device=dev) for name, Nr, Kr, N, K, kind, qg in plan}
+    lin = []
+    for l in range(layers):
+        for (p, s0), (name, Nr, Kr, N, K, kind, qg) in zip(packed[l], plan):
+            lin.append((X[qg], p, s0, N, Y[name], K))
+    chunks = [lin[i:i + 128] for i in range(0, len(lin), 128)]
+    ws = qoq.Workspace(dev)
+
+    def run():
+        for c in chunks:
+            qoq.w4a8_linear_chain(c, workspace=ws, stream=stream)
+
+    with torch.cuda.stream(stream):
+        run()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            run()
+        steps = max(10, args.steps // 2)
+        ms = timed(g, steps, 3) / steps
+    del Y
+    return {"value": step_bytes / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "launches_per_step": len(chunks),
+            "what": "same decode step in one persistent kernel per <= 128 linears (qoq_w4a8_linear_chain): "
+                    "in-kernel per-token quantization, k-split / stream-K over all SMs, grid-wide ordering"}
+
+
+def sweep_measure(qoq, torch, args, plan, packed, layers, dev, stream, timed, Ms=(1, 2, 4, 8, 16, 32, 64, 128, 256)):
+    """BASELINE config C2: the decode step (quantizer + W4A8 GEMM per linear, one CUDA graph) over the
+    decode token counts M = 1 .. 256, GB/s of the §8(d) algorithmic bytes and TOPS."""
+    out = {}
+    gen = torch.Generator(device=dev)
+    for M in Ms:
+        gen.manual_seed(70 + M)
+        Xs = {}
+        for name, Nr, Kr, N, K, kind, qg in plan:
+            Xs[qg] = synth.device_activations_fp16(M, K, gen, dev)
+        qo = {qg: (torch.empty(M, x.shape[1], dtype=torch.int8, device=dev), torch.empty(M, dtype=torch.float16, device=dev),
+                   torch.empty(M, dtype=torch.int32, device=dev)) for qg, x in Xs.items()}
+        Ys = {name: torch.empty(M, Nr, dtype=torch.float16, device=dev) for name, Nr, Kr, N, K, kind, qg in plan}
+        wsm = qoq.Workspace(dev)
+        wsm.get(max(qoq.gemm_workspace_bytes(M, Nr, Kr) for name, Nr, Kr, N, K, kind, qg in plan))
+
+        def run():
+            for l in range(layers):
+                done = set()
+                for (p, s0), (name, Nr, Kr, N, K, kind, qg) in zip(packed[l], plan):
+                    if qg not in done:
+                        qoq.quantize_activations_per_token(Xs[qg], out=qo[qg], stream=stream)
+                        done.add(qg)
+                    qx, sx, tx = qo[qg]
+                    qoq.w4a8_gemm(qx, sx, tx, p, s0, Nr, out=Ys[name], workspace=wsm, stream=stream)
+
+        with torch.cuda.stream(stream):
+            run()
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                run()
+            steps = 10
+            ms = timed(g, steps, 3) / steps
+        nb, ops = step_work(args.model, M, layers, 1, not args.unfused_gate_up)
+        out[str(M)] = {"ms_per_step": ms, "GBps": nb / (ms * 1e-3) / 1e9, "TOPS": ops / (ms * 1e-3) / 1e12}
+        del g, Xs, qo, Ys
+    return out
 
 
 def per_channel_measure(qoq, torch, args, shapes, layers, dev, stream, X, quant_out, Ybuf, ws, timed):
@@ -724,10 +860,11 @@ def kv4_measure(qoq, torch, dev, stream, timed, B=64, T=1024, H=32, H_kv=8, D=12
             "paper_context": "A100 QServe KV4 kernel 0.28 ms at seq 1024 (Table P:507-526; other GPU/model: context only)"}
 
 
-def prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream):
+def prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream, M=None, with_ceiling=True):
     """Tensor-bound regime (BASELINE configs[2]): GEMM-only TOPS at M = prefill_M over the first
-    4 layers' weights (rotating, > L2), and the INT8 ceiling measured with cuBLASLt in the same run."""
-    M = args.prefill_M
+    4 layers' weights (rotating, > L2), per projection, and the INT8 ceiling measured with cuBLASLt in
+    the same run."""
+    M = args.prefill_M if M is None else M
     L = min(4, layers)
     gen = torch.Generator(device=dev)
     gen.manual_seed(11)
@@ -766,8 +903,32 @@ def prefill_measure(qoq, torch, args, shapes, packed, layers, dev, stream):
     ms = e0.elapsed_time(e1) / reps
     ops = sum(gemm_ops(M, N, K) for _, N, K, _, _ in shapes) * L
     tops = ops / (ms * 1e-3) / 1e12
-    ceil = int8_ceiling(torch, dev)
-    return {"M": M, "layers": L, "tops": tops, "ms": ms,
+    per = {}
+    with torch.cuda.stream(stream):   # each projection alone (rotating over the L layers' weights)
+        for i, (name, N, K, kind, qg) in enumerate(shapes):
+            qx, sx, tx = q[K]
+
+            def one():
+                for l in range(L):
+                    p, s0 = packed[l][i]
+                    qoq.w4a8_gemm(qx, sx, tx, p, s0, N, out=Y[name], workspace=ws, stream=stream)
+
+            one()
+            g1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1, stream=stream):
+                one()
+            g1.replay()
+            stream.synchronize()
+            e0.record(stream)
+            for _ in range(reps):
+                g1.replay()
+            e1.record(stream)
+            stream.synchronize()
+            t1 = e0.elapsed_time(e1) / reps / L
+            per[name] = gemm_ops(M, N, K) / (t1 * 1e-3) / 1e12
+    ceil = int8_ceiling(torch, dev) if with_ceiling else None
+    del q, Y
+    return {"M": M, "layers": L, "tops": tops, "ms": ms, "per_gemm_tops": per,
             "frac_int8_datasheet": tops / INT8_DATASHEET_TOPS,
             "int8_ceiling_tops": ceil, "frac_int8_measured_ceiling": tops / ceil if ceil else None,
             "ceiling_how": "torch._int_mm (cuBLASLt IMMA) 8192^3 best of 10, same run"}

@@ -59,6 +59,7 @@ def lib() -> ctypes.CDLL:
                 "oracle_epilogue_f64": (I, [P, P, P, I, I, P]),
                 "oracle_linear_rows": (I, [P, I, I, I, I, P, P, I, P]),
                 "oracle_num_threads": (I, []),
+                "oracle_set_num_threads": (None, [I]),
                 "oracle_pc_quantize": (I, [P, I, I, P, P, P]),
                 "oracle_pc_pack": (I, [P, I, I, P]),
                 "oracle_pc_unpack": (I, [P, I, I, P]),
@@ -243,6 +244,10 @@ def linear_rows(X: np.ndarray, packed: np.ndarray, s0: np.ndarray, N: int,
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    lib().oracle_set_num_threads(int(n))
 
 
 # ---- NEXT-1: per-channel W4A8 (§5.2.2) ----

@@ -20,6 +20,15 @@
 #define TILE_K 128
 #define TILE_BYTES 8448 /* 8192 packed nibbles + 128 s_u8 + 128 z*s_u8 */
 
+/* Thread count of the OpenMP GEMM loops (bench.py times the oracle single-threaded and on all cores). */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -147,6 +147,7 @@ int oracle_attention_f64(const uint16_t* Q, const double* Khat, const double* Vh
 
 /* Number of OpenMP threads the oracle's parallel loops use (1 without OpenMP). */
 int oracle_num_threads(void);
+void oracle_set_num_threads(int n);
 
 #ifdef __cplusplus
 }

@@ -167,8 +167,11 @@ def quantize_activations_per_token(X: torch.Tensor, K: int | None = None, want_t
     """X [M][ldx] fp16 -> (qx int8 [M][K], sx fp16 [M], tx int32 [M] or None)."""
     if X.dtype != torch.float16 or X.dim() != 2:
         raise ValueError("X must be a 2-D fp16 tensor")
-    M, ldx = X.shape
-    K = ldx if K is None else K
+    if X.stride(1) != 1 or not X.is_cuda:
+        raise ValueError("X must be a CUDA tensor with contiguous rows")
+    M = X.shape[0]
+    ldx = X.stride(0) if M > 1 else X.shape[1]     # a row-strided view (e.g. a TP K-shard) is fine
+    K = X.shape[1] if K is None else K
     if out is None:
         qx = torch.empty(M, K, dtype=torch.int8, device=X.device)
         sx = torch.empty(M, dtype=torch.float16, device=X.device)
@@ -176,8 +179,8 @@ def quantize_activations_per_token(X: torch.Tensor, K: int | None = None, want_t
     else:
         qx, sx, tx = out
     _check("qoq_quantize_activations_per_token",
-           load().qoq_quantize_activations_per_token(_ptr(X), M, K, ldx, _ptr(qx), _ptr(sx), _ptr(tx),
-                                                     _stream(stream)))
+           load().qoq_quantize_activations_per_token(ctypes.c_void_p(X.data_ptr()), M, K, ldx, _ptr(qx), _ptr(sx),
+                                                     _ptr(tx), _stream(stream)))
     return qx, sx, tx
 
 

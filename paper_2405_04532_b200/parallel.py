@@ -106,3 +106,71 @@ def tp_mlp(X, gate_up_shard, down_shard, linear, act_linear, all_reduce, rank: i
     if world > 1:
         all_reduce(Y)
     return Y
+
+
+# ------------------------------------------------------------------ the decode step's layer under TP
+# (one code path for bench.py on GPUs and tests/test_tp_gloo.py on CPU)
+
+QUANT_GROUP = {"qkv": "attn_in", "o": "attn_out", "gate": "mlp_in", "up": "mlp_in", "gate_up": "mlp_in",
+               "down": "mlp_act"}
+
+
+def rank_layer_plan(shapes, world: int):
+    """Per-rank GEMMs of one layer: [(name, N_r, K_r, N, K, kind, quant_group)] for the model's
+    [(name, N, K, kind)] (gate and up possibly fused into gate_up). Column-parallel layers split N,
+    row-parallel layers split K, both at 128 boundaries; quant_group names the activation quantization
+    that feeds the GEMM (gate and up share one, Fig. 7)."""
+    out = []
+    for name, N, K, kind in shapes:
+        check_shardable(N // 2 if name == "gate_up" else N, K, kind, world)
+        Nr, Kr = (N // world, K) if kind == "col" else (N, K // world)
+        out.append((name, Nr, Kr, N, K, kind, QUANT_GROUP[name]))
+    return out
+
+
+def shard_packed_gate_up(packed, s0, I: int, K: int, rank: int, world: int):
+    """The rank's shard of a fused, packed [gate; up] weight (N = 2I): the tiles of gate rows [a, b) then
+    those of up rows [a, b) (gate_up_shard_rows), so the rank's output is [gate_r | up_r]."""
+    a, b = gate_up_shard_rows(I, rank, world)
+    NT, KT = 2 * I // GROUP, K // GROUP
+    tiles = packed.reshape(NT, KT, TILE_BYTES)
+    ga, gb, ua, ub = a // GROUP, b // GROUP, (I + a) // GROUP, (I + b) // GROUP
+    if hasattr(tiles, "contiguous"):      # torch
+        import torch
+        p = torch.cat([tiles[ga:gb], tiles[ua:ub]]).reshape(-1)
+        s = torch.cat([s0[a:b], s0[I + a:I + b]])
+    else:                                 # numpy
+        import numpy as np
+        p = np.concatenate([tiles[ga:gb], tiles[ua:ub]]).reshape(-1)
+        s = np.concatenate([s0[a:b], s0[I + a:I + b]])
+    return p, s
+
+
+def shard_layer(packed_layer, plan, rank: int, world: int):
+    """Per-rank shards [(packed_r, s0_r)] of one layer's full packed weights [(packed, s0)] (quantize once
+    on the full weight, then distribute: the same quantized weights as 1 GPU)."""
+    out = []
+    for (packed, s0), (name, Nr, Kr, N, K, kind, qg) in zip(packed_layer, plan):
+        if world == 1:
+            out.append((packed, s0))
+        elif name == "gate_up" and kind == "col":
+            out.append(shard_packed_gate_up(packed, s0, N // 2, K, rank, world))
+        else:
+            out.append(shard_packed(packed, s0, N, K, kind, rank, world))
+    return out
+
+
+def tp_decode_layer(inputs, shards, plan, linear, all_reduce, rank: int, world: int):
+    """One decode layer of the benchmark step on this rank, in order (qkv, o, gate_up, down):
+    X = inputs[quant_group] (replicated [M][K]; a row-parallel rank reads its K-shard view), then
+    Y = linear(X_r, shard, plan_entry) (quantize X_r per token + W4A8 GEMM), then one all_reduce of Y after
+    each row-parallel linear. Returns {name: Y}."""
+    out = {}
+    for shard, entry in zip(shards, plan):
+        name, Nr, Kr, N, K, kind, qg = entry
+        X_r = shard_input(inputs[qg], kind, rank, world)
+        Y = linear(X_r, shard, entry)
+        if kind == "row" and world > 1:
+            all_reduce(Y)
+        out[name] = Y
+    return out

@@ -221,3 +221,95 @@ def test_tp_mlp_gloo_fused_silu_quant():
     assert np.array_equal(res[0][1].view(np.uint16), res[1][1].view(np.uint16))   # all ranks agree
     y = res[0][1].astype(np.float64)
     assert np.all(np.abs(y - ref) <= RTOL * np.abs(ref) + ATOL)
+
+
+# ---- the benchmark step's own TP path (parallel.rank_layer_plan / shard_layer / tp_decode_layer: the
+# functions bench.py runs on GPUs) over gloo, world 2, with the oracle as the rank-local linear ----
+
+TINY = [("qkv", 512, 256, "col"), ("o", 256, 256, "row"), ("gate", 512, 256, "col"), ("up", 512, 256, "col"),
+        ("down", 256, 512, "row")]
+
+
+def _step_inputs(M):
+    shapes = synth.fuse_gate_up(TINY)
+    Ks = {parallel.QUANT_GROUP[n]: K for n, N, K, kind in shapes}
+    return shapes, {qg: synth.activations_fp16(M, K, seed=11 + K) for qg, K in Ks.items()}
+
+
+def _step_weights(shapes):
+    """Full weights, quantized once (oracle packer); gate_up is the fused [gate; up] weight."""
+    out = []
+    for i, (name, N, K, kind) in enumerate(shapes):
+        W = synth.weights_fp16(N, K, seed=40 + i, std_scale=0.25)
+        out.append(oracle.quantize_weights(W))
+    return out
+
+
+def _step_linear(X_r, shard, entry):
+    name, Nr, Kr, N, K, kind, qg = entry
+    p, s0 = shard
+    return _oracle_linear(np.ascontiguousarray(X_r), (np.ascontiguousarray(p), np.ascontiguousarray(s0), Nr))
+
+
+def _step_worker(rank, world, port, M, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shapes, inputs = _step_inputs(M)
+        plan = parallel.rank_layer_plan(shapes, world)
+        shards = parallel.shard_layer(_step_weights(shapes), plan, rank, world)
+
+        def all_reduce(Y):
+            dist.all_reduce(Y, op=dist.ReduceOp.SUM)
+
+        out = parallel.tp_decode_layer(inputs, shards, plan, _step_linear, all_reduce, rank, world)
+        out_q.put((rank, {k: v.numpy() for k, v in out.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_step_tp_path_gloo():
+    """bench.py's decode layer at TP = 2 (gloo, oracle per rank): qkv / gate_up column shards are
+    bit-identical to the 1-GPU result on their rows ([gate_r | up_r] for the fused gate_up), o / down are
+    all-reduced fp16 partials within tolerance of the fp64 sum of the per-rank exact results, every rank
+    ends with the same reduced outputs, and TP = 1 through the same function reproduces the 1-GPU layer."""
+    M, world = 8, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, world, port, M, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shapes, inputs = _step_inputs(M)
+    full = _step_weights(shapes)
+    plan1 = parallel.rank_layer_plan(shapes, 1)
+    one = {k: v.numpy() for k, v in parallel.tp_decode_layer(inputs, parallel.shard_layer(full, plan1, 0, 1), plan1,
+                                                            _step_linear, None, 0, 1).items()}
+    # column-parallel: bit-identical slices
+    a0 = one["qkv"].shape[1] // 2
+    assert np.array_equal(np.concatenate([res[0]["qkv"], res[1]["qkv"]], 1).view(np.uint16), one["qkv"].view(np.uint16))
+    I = one["gate_up"].shape[1] // 2
+    for r in range(world):
+        a, b = parallel.gate_up_shard_rows(I, r, world)
+        gu = res[r]["gate_up"]
+        assert np.array_equal(gu[:, : b - a].view(np.uint16), one["gate_up"][:, a:b].view(np.uint16))
+        assert np.array_equal(gu[:, b - a:].view(np.uint16), one["gate_up"][:, I + a:I + b].view(np.uint16))
+    # row-parallel: all ranks agree; within tolerance of the exact per-rank sum; close to 1 GPU
+    plan2 = parallel.rank_layer_plan(shapes, world)
+    for name in ("o", "down"):
+        assert np.array_equal(res[0][name].view(np.uint16), res[1][name].view(np.uint16))
+        i = [e[0] for e in plan2].index(name)
+        ref = 0
+        for r in range(world):
+            p_r, s0_r = parallel.shard_layer(full, plan2, r, world)[i]
+            X_r = np.ascontiguousarray(parallel.shard_input(inputs[plan2[i][6]], "row", r, world))
+            ref = ref + oracle.linear_rows(X_r, p_r, s0_r, plan2[i][1])
+        y = res[0][name].astype(np.float64)
+        assert np.all(np.abs(y - ref) <= RTOL * np.abs(ref) + ATOL), name
+        assert np.linalg.norm(y - one[name]) / np.linalg.norm(one[name]) < 0.05
+    assert a0 > 0
