@@ -5,11 +5,12 @@
 //                            point — the per-channel rule of Q20-Q22 — and written into the sequence's
 //                            page slot ("dynamic", "updated on-the-fly").
 //   kv4_decode_attn_kernel : o_h = softmax(q_h K̂ᵀ/√D) V̂ for every query head h sharing kv head g (GQA),
-//                            a cluster of 4 CTAs per (sequence, kv head), 8 warps each striding over chunks
-//                            of 32/R tokens (butterfly-reduced scores, online softmax in fp32), the 32 warp
-//                            states merged by CTA 0 through distributed shared memory.
-// Dequantization (q − z)·s is exact in fp32 (an 11-bit scale times an integer in [−15, 15]); the paper's
-// FP16 arithmetic was an A100 CUDA-core roofline measure that B200 does not need.
+//                            a cluster of QOQ_KV4_SPLIT CTAs per (sequence, kv head) splitting its pages,
+//                            4 warps each taking 16-token chunks on tensor cores (mma.sync m16n8k16,
+//                            fp32 accumulation, online softmax in base 2), the warp states merged by CTA 0
+//                            through distributed shared memory.
+// The dequantization (q − z)·s is folded out of both contractions: the tensor cores multiply exact fp16
+// integers (q − z) and the scales are applied to the fp32 results (QK) or to the probabilities (PV).
 #include <cooperative_groups.h>
 #include <cuda_fp16.h>
 #include <cstdint>
@@ -20,18 +21,18 @@
 namespace qoq {
 
 constexpr int kKvD = 128;       // head dim (Llama / Qwen families)
-constexpr int kAttnWarps = 8;
+constexpr int kAttnWarps = 4;   // a warp takes 16-token chunks of the staged pages
 #ifndef QOQ_KV4_SPLIT
 #define QOQ_KV4_SPLIT 2
 #endif
 constexpr int kAttnSplit = QOQ_KV4_SPLIT;
 #ifndef QOQ_KV4_MINB
-#define QOQ_KV4_MINB 2   // CTAs per SM the register budget is sized for
+#define QOQ_KV4_MINB 4   // CTAs per SM the register budget is sized for (4: 128 registers, measured best)
 #endif
 #ifndef QOQ_KV4_STAGES
 #define QOQ_KV4_STAGES 3
 #endif
-constexpr int kKvStages = QOQ_KV4_STAGES;    // pages in flight per CTA (TMA bulk copies into shared memory)   // CTAs (one thread-block cluster) per (sequence, kv head), merged over DSMEM
+constexpr int kKvStages = QOQ_KV4_STAGES;    // pages in flight per CTA (TMA bulk copies into shared memory)
 
 __device__ __forceinline__ size_t kv_head_bytes(int P) { return (size_t)P * (kKvD + 8); }
 
@@ -81,59 +82,84 @@ __global__ void __launch_bounds__(64) kv4_append_kernel(const __half* __restrict
     }
 }
 
-// 4 codes of one 16-bit word -> (q - z) * s, exact in fp32
-__device__ __forceinline__ void dequant4(uint32_t c, float s, float zs, float (&v)[4]) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = __fmaf_rn((float)((c >> (4 * i)) & 15u), s, zs);   // q s - z s: exact
+// ------------------------------------------------------------------ decode attention on tensor cores
+//
+// Per warp, a chunk of 16 tokens of one staged page; the GQA group's R query heads are the MMA rows
+// (padded to 16), so both contractions run as mma.sync.m16n8k16 (fp16 inputs, fp32 accumulation):
+//   S[h][t] = Σ_d q[h][d] · (c_K[t][d] − z_K[t])           (QK: A = q, B = integer codes − zero point)
+//   score    = S · s_K[t] · log2(e)/√D                       (the scale folded out of the dot product)
+//   O[h][d] += Σ_t (p[h][t] · s_V[t]) · (c_V[t][d] − z_V[t]) (PV: A = p·s_V split hi + lo in fp16,
+//                                                             B = integer codes − zero point)
+// Every fp16 input is exact: q as given, c − z ∈ [−15, 15], and p·s_V carried as two fp16 terms (≈ 22
+// significant bits), so the only roundings are the fp32 accumulations — the error model of
+// tests/kv4_tol.py. The QK accumulator fragment of two 8-token blocks IS the PV A fragment (heads ×
+// tokens), so scores never leave registers. Online softmax in base 2 per head (a quad of lanes).
+
+// mma.sync m16n8k16, row.col, f16 x f16 -> f32, accumulating rows gq (d0, d1) in place. A's rows gq + 8
+// are always zero here (padding heads), so their accumulators (p2, p3) stay 0 — one scratch pair shared by
+// every call (the B operands are finite integers, so 0·B adds exact zeros).
+__device__ __forceinline__ void mma16816(float& d0, float& d1, float& p2, float& p3, uint32_t a0, uint32_t a2,
+                                         uint32_t b0, uint32_t b1) {
+    asm(   // not volatile: a pure function of its operands, so the scheduler may interleave independent chains
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d0), "+f"(d1), "+f"(p2), "+f"(p3)
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
 
-// Each warp walks its sequence in chunks of C = 32 / R tokens. For one chunk a lane (owning dims
-// 4l..4l+3) forms the 32 partial dot products (token c, head j) from its 4 dequantized K values; one
-// butterfly reduce-scatter (31 shuffles) leaves lane L with the full score of (c, j) = (L / R, L % R).
-// The chunk's softmax update runs on those lanes (max over the lanes of one head, one exp2 each), the
-// 32 probabilities are broadcast back by shuffles and the lane accumulates p · v̂ for its 4 dims.
+// Codes to exact fp16 (c − z) with 3 instructions per half2: PRMT places the code bytes under 0x64 high
+// bytes, LOP3 keeps one nibble per half (0x6400 | c = 1024 + c, or 0x6400 | 16c = 1024 + 16c), and one
+// HFMA2 scales by (1 or 1/16) and subtracts (1024 + z or 64 + z): every step is exact in fp16.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+__device__ __forceinline__ uint32_t hfma2_bits(uint32_t x, uint32_t m, uint32_t c) {
+    const __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&x), *reinterpret_cast<const __half2*>(&m),
+                              *reinterpret_cast<const __half2*>(&c));
+    return *reinterpret_cast<const uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t h2bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
 template <int R>
 __global__ void __launch_bounds__(kAttnWarps * 32, QOQ_KV4_MINB) kv4_decode_attn_kernel(
     const __half* __restrict__ Q, const uint8_t* __restrict__ pages, const int32_t* __restrict__ block_table,
     const int32_t* __restrict__ seq_lens, int H_kv, int P, int max_pages, __half* __restrict__ O) {
-    constexpr int C = 32 / R;
+    static_assert(R >= 1 && R <= 8, "GQA group of <= 8 query heads (MMA rows 0..7)");
     __shared__ float sm_m[kAttnWarps][R], sm_l[kAttnWarps][R];
     __shared__ float sm_acc[kAttnWarps][R][kKvD];
     pdl_wait();
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
-    const int b = blockIdx.x, g = blockIdx.y, l = threadIdx.x & 31;
-    // warp index via a lane-0 broadcast: provably warp-uniform, so the token loop (and the shuffles in
-    // it) need no per-shuffle reconvergence code
+    const int b = blockIdx.x, g = blockIdx.y, lane = threadIdx.x & 31;
     const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-    const int rank = (int)cluster.block_rank();           // = blockIdx.z: this CTA's share of the tokens
+    const int rank = (int)cluster.block_rank();
     const int H = H_kv * R;
     const int T = seq_lens[b];
-    const float qscale = 1.4426950408889634f / sqrtf((float)kKvD);   // log2(e) / sqrt(D): scores in base 2
-    float qf[R][4];
+    const int gq = lane >> 2, tq = lane & 3;              // fragment row group / thread in quad
+    const float qscale = 1.4426950408889634f / sqrtf((float)kKvD);
+    // A fragments of q (rows = heads gq; rows gq + 8 are padding): a0a1 (d = 16kb + 2tq), a4a5 (+8)
+    uint32_t qa[8][2];
+    {
+        const bool real = gq < R;
+        const __half* qrow = Q + ((size_t)b * H + (size_t)g * R + (real ? gq : 0)) * kKvD;
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-        const uint2 raw = reinterpret_cast<const uint2*>(Q + ((size_t)b * H + (size_t)g * R + j) * kKvD)[l];
-        const __half* h = reinterpret_cast<const __half*>(&raw);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) qf[j][i] = __half2float(h[i]) * qscale;
+        for (int kb = 0; kb < 8; ++kb) {
+            qa[kb][0] = real ? *reinterpret_cast<const uint32_t*>(qrow + 16 * kb + 2 * tq) : 0u;
+            qa[kb][1] = real ? *reinterpret_cast<const uint32_t*>(qrow + 16 * kb + 2 * tq + 8) : 0u;
+        }
     }
-    float m[R], lsum[R], acc[R][4];
+    float o[16][2];                                        // O fragments: (head gq, d = 8nb + 2tq, +1)
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-        m[j] = -INFINITY;
-        lsum[j] = 0.0f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[j][i] = 0.0f;
-    }
+    for (int nb = 0; nb < 16; ++nb) o[nb][0] = o[nb][1] = 0.0f;
+    float pad2 = 0.0f, pad3 = 0.0f;                        // the padding rows' accumulators (stay 0)
+    float m = -INFINITY, lsum = 0.0f;                      // online softmax state of head gq (base 2)
     const size_t hb = kv_head_bytes(P), pb = (size_t)H_kv * hb;
     const int32_t* bt = block_table + (size_t)b * max_pages;
-    const int myc = l / R, myj = l % R;
-    // TMA pipeline: the (page, kv head) slice — K codes, V codes, (s, z) pairs: P·(D+8) contiguous bytes —
-    // arrives in shared memory by one cp.async.bulk per page, kKvStages pages ahead of the warps.
     extern __shared__ __align__(16) uint8_t stage_buf[];
     __shared__ __align__(8) uint64_t full_bar[kKvStages];
-    const int NP = (T + P - 1) / P;                        // pages of this sequence
+    const int NP = (T + P - 1) / P;
     const int my_pages = NP > rank ? (NP - rank + kAttnSplit - 1) / kAttnSplit : 0;
     if (threadIdx.x == 0) {
         for (int i = 0; i < kKvStages; ++i) mbar_init(&full_bar[i], 1);
@@ -148,73 +174,135 @@ __global__ void __launch_bounds__(kAttnWarps * 32, QOQ_KV4_MINB) kv4_decode_attn
                      (uint32_t)hb, &full_bar[n], policy);
         }
     }
+    const uint32_t ksel = 0x4040u | (0x0101u * (uint32_t)tq);   // PRMT: bytes (w.tq, 0x64, w.tq, 0x64)
+    const uint32_t kscale = 0x2C003C00u;                   // half2 (1, 1/16)
+    // V: nibble (gq & 1) of byte (gq >> 1) of word nb, for two tokens: PRMT (w0.byte, -, w1.byte, -), keep the
+    // nibble, OR in the 0x64 high bytes
+    const uint32_t vsel = (uint32_t)(gq >> 1) | ((4u + (gq >> 1)) << 8);
+    const uint32_t vmask = (gq & 1) ? 0x00F000F0u : 0x000F000Fu;
+    const uint32_t vscale = (gq & 1) ? 0x2C002C00u : 0x3C003C00u;   // (1/16, 1/16) or (1, 1)
+    const float vbase = (gq & 1) ? 64.0f : 1024.0f;
     for (int n = 0; n < my_pages; ++n) {
         const int stg = n % kKvStages;
         mbar_wait(&full_bar[stg], (uint32_t)((n / kKvStages) & 1));
         const uint8_t* base = stage_buf + (size_t)stg * hb;
+        const uint32_t* par = reinterpret_cast<const uint32_t*>(base + (size_t)P * kKvD);   // (s, z) fp16 pairs
         const int tp = (rank + kAttnSplit * n) * P;        // first token of this page
-        for (int o0 = w * C; o0 < P; o0 += kAttnWarps * C) {
-            const int t0 = tp + o0;
-            if (t0 >= T) break;
-            uint32_t kc[C], vc[C], kp[C], vp[C];           // codes (16 bits), (s, z) fp16 pairs
+        for (int o0 = 16 * w; o0 < P; o0 += 16 * kAttnWarps) {
+            if (tp + o0 >= T) break;
+            const int valid = T - (tp + o0);               // tokens of this chunk that exist (>= 1)
+            // ---- S = q (c_K − z_K)ᵀ for the two 8-token blocks (two independent MMA chains, interleaved);
+            // C fragment: (head gq, tokens 8nbt + 2tq, +1)
+            float sc[2][4];
+            {
+                const uint4* row0 = reinterpret_cast<const uint4*>(base + (size_t)(o0 + gq) * (kKvD / 2));
+                const uint4* row1 = reinterpret_cast<const uint4*>(base + (size_t)(o0 + 8 + gq) * (kKvD / 2));
+                // c = (lo, hi) of byte tq of a word: (1024 + lo, 1024 + 16 hi) -> (lo − z, hi − z)
+                const __half z0 = __ushort_as_half((unsigned short)(par[o0 + gq] >> 16));       // fp16 z (integer)
+                const __half z1 = __ushort_as_half((unsigned short)(par[o0 + 8 + gq] >> 16));
+                const uint32_t zb0 = h2bits(__halves2half2(__hneg(__hadd(__float2half(1024.0f), z0)),
+                                                           __hneg(__hadd(__float2half(64.0f), z0))));
+                const uint32_t zb1 = h2bits(__halves2half2(__hneg(__hadd(__float2half(1024.0f), z1)),
+                                                           __hneg(__hadd(__float2half(64.0f), z1))));
+                float acc0[2] = {0.0f, 0.0f}, acc1[2] = {0.0f, 0.0f};
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                const bool in = t0 + c < T;
-                kc[c] = in ? reinterpret_cast<const uint16_t*>(base + (size_t)(o0 + c) * (kKvD / 2))[l] : 0u;
-                vc[c] = in ? reinterpret_cast<const uint16_t*>(base + (size_t)(P + o0 + c) * (kKvD / 2))[l] : 0u;
-                kp[c] = in ? reinterpret_cast<const uint32_t*>(base + (size_t)P * kKvD)[o0 + c] : 0u;
-                vp[c] = in ? reinterpret_cast<const uint32_t*>(base + (size_t)P * kKvD)[P + o0 + c] : 0u;
+                for (int qd = 0; qd < 4; ++qd) {           // 16 words of each code row, 4 at a time
+                    const uint4 w0 = row0[qd], w1 = row1[qd];
+                    const uint32_t x0[4] = {w0.x, w0.y, w0.z, w0.w}, x1[4] = {w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {       // kb = 2 qd + h2: words 2kb (d 16kb+2tq..) and 2kb+1 (+8)
+                        const int kb = 2 * qd + h2;
+                        const uint32_t b00 = hfma2_bits(prmt(x0[2 * h2], 0x64646464u, ksel) & 0xFFF0FF0Fu, kscale, zb0);
+                        const uint32_t b01 = hfma2_bits(prmt(x0[2 * h2 + 1], 0x64646464u, ksel) & 0xFFF0FF0Fu, kscale, zb0);
+                        const uint32_t b10 = hfma2_bits(prmt(x1[2 * h2], 0x64646464u, ksel) & 0xFFF0FF0Fu, kscale, zb1);
+                        const uint32_t b11 = hfma2_bits(prmt(x1[2 * h2 + 1], 0x64646464u, ksel) & 0xFFF0FF0Fu, kscale, zb1);
+                        mma16816(acc0[0], acc0[1], pad2, pad3, qa[kb][0], qa[kb][1], b00, b01);
+                        mma16816(acc1[0], acc1[1], pad2, pad3, qa[kb][0], qa[kb][1], b10, b11);
+                    }
+                }
+                // scores of tokens 8nbt + 2tq, +1 for head gq
+#pragma unroll
+                for (int nbt = 0; nbt < 2; ++nbt)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int tt = 8 * nbt + 2 * tq + u;
+                        const float sk = __half2float(__ushort_as_half((unsigned short)(par[o0 + tt] & 0xFFFFu)));
+                        sc[nbt][u] = tt < valid ? (nbt ? acc1[u] : acc0[u]) * sk * qscale : -INFINITY;
+                    }
             }
-            float v[32];
+            // ---- online softmax for head gq over this chunk's 16 tokens (4 per lane of the quad)
+            float cm = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
+            cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+            cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+            const float mnew = fmaxf(m, cm);
+            const float corr = (m == -INFINITY) ? 0.0f : exp2f(m - mnew);
+            float pv[2][2], ps = 0.0f;
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                float kh[4];
-                const float2 k2 = __half22float2(*reinterpret_cast<const __half2*>(&kp[c]));
-                dequant4(kc[c], k2.x, -k2.y * k2.x, kh);
+            for (int nbt = 0; nbt < 2; ++nbt)
 #pragma unroll
-                for (int j = 0; j < R; ++j)
-                    v[c * R + j] = qf[j][0] * kh[0] + qf[j][1] * kh[1] + qf[j][2] * kh[2] + qf[j][3] * kh[3];
-            }
-            // butterfly reduce-scatter: lane L ends with the warp sum of v[L]
+                for (int u = 0; u < 2; ++u) {
+                    pv[nbt][u] = sc[nbt][u] == -INFINITY ? 0.0f : exp2f(sc[nbt][u] - mnew);
+                    ps += pv[nbt][u];
+                }
+            ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+            ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+            lsum = lsum * corr + ps;
+            m = mnew;
+            if (__any_sync(0xffffffffu, corr != 1.0f)) {   // the running max moved for some head
 #pragma unroll
-            for (int st = 16; st >= 1; st >>= 1) {
-                const bool up = (l & st) != 0;
-#pragma unroll
-                for (int i = 0; i < st; ++i) {
-                    const float send = up ? v[i] : v[i + st];
-                    const float keep = up ? v[i + st] : v[i];
-                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+                for (int nb = 0; nb < 16; ++nb) {
+                    o[nb][0] *= corr;
+                    o[nb][1] *= corr;
                 }
             }
-            const float sc = (t0 + myc < T) ? v[0] : -INFINITY;
-            float cm = sc;                                          // chunk max over the lanes of head myj
+            // ---- PV: A = p · s_V (hi + lo fp16) for tokens (2tq, 2tq+1) and (8 + 2tq, 9 + 2tq)
+            uint32_t ahi[2], alo[2];
 #pragma unroll
-            for (int x = R; x < 32; x <<= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, x));
-            float mj = m[0];
+            for (int nbt = 0; nbt < 2; ++nbt) {
+                float f[2];
 #pragma unroll
-            for (int j = 1; j < R; ++j) mj = (myj == j) ? m[j] : mj;
-            const float mnew = fmaxf(mj, cm);
-            const float p = (sc == -INFINITY) ? 0.0f : exp2f(sc - mnew);
-            const float corr = (mj == -INFINITY) ? 0.0f : exp2f(mj - mnew);
-#pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const float cj = __shfl_sync(0xffffffffu, corr, j);
-                m[j] = __shfl_sync(0xffffffffu, mnew, j);
-                lsum[j] *= cj;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) acc[j][i] *= cj;
+                for (int u = 0; u < 2; ++u) {
+                    const int tt = 8 * nbt + 2 * tq + u;
+                    const float sv = __half2float(__ushort_as_half((unsigned short)(par[P + o0 + tt] & 0xFFFFu)));
+                    f[u] = pv[nbt][u] * sv;
+                }
+                const __half2 hi = __floats2half2_rn(f[0], f[1]);
+                const float2 hf = __half22float2(hi);
+                ahi[nbt] = h2bits(hi);
+                alo[nbt] = h2bits(__floats2half2_rn(f[0] - hf.x, f[1] - hf.y));
             }
+            // B fragments: V codes of tokens 2tq, 2tq+1 (b0) and 8+2tq, 9+2tq (b1) at d = 8nb + gq
+            const uint4* vr[4];
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                float vh[4];
-                const float2 v2 = __half22float2(*reinterpret_cast<const __half2*>(&vp[c]));
-                dequant4(vc[c], v2.x, -v2.y * v2.x, vh);
+            for (int i = 0; i < 4; ++i) {
+                const int tt = (i < 2 ? 0 : 8) + 2 * tq + (i & 1);
+                vr[i] = reinterpret_cast<const uint4*>(base + (size_t)(P + o0 + tt) * (kKvD / 2));
+            }
+            uint32_t vb[2];                                // −(base + z) of the two tokens of each pair
 #pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const float pc = __shfl_sync(0xffffffffu, p, c * R + j);
-                    lsum[j] += pc;
+            for (int pr = 0; pr < 2; ++pr) {
+                const int t0 = 8 * pr + 2 * tq;
+                const __half z0 = __ushort_as_half((unsigned short)(par[P + o0 + t0] >> 16));
+                const __half z1 = __ushort_as_half((unsigned short)(par[P + o0 + t0 + 1] >> 16));
+                vb[pr] = h2bits(__halves2half2(__hneg(__hadd(__float2half(vbase), z0)), __hneg(__hadd(__float2half(vbase), z1))));
+            }
+            // masked tokens (past the sequence end, only in its last chunk) take p = 0 and code = z (no
+            // NaN / Inf from never-written page bytes)
+            const bool full = valid >= 16;
+            const uint32_t keep0 = full ? 0xFFFFFFFFu : ((2 * tq < valid ? 0xFFFFu : 0u) | (2 * tq + 1 < valid ? 0xFFFF0000u : 0u));
+            const uint32_t keep1 = full ? 0xFFFFFFFFu : ((8 + 2 * tq < valid ? 0xFFFFu : 0u) | (9 + 2 * tq < valid ? 0xFFFF0000u : 0u));
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[j][i] = __fmaf_rn(pc, vh[i], acc[j][i]);
+            for (int q4 = 0; q4 < 4; ++q4) {               // words 4 q4 .. 4 q4 + 3 of the four code rows
+                const uint4 r0 = vr[0][q4], r1 = vr[1][q4], r2 = vr[2][q4], r3 = vr[3][q4];
+                const uint32_t a0[4] = {r0.x, r0.y, r0.z, r0.w}, a1[4] = {r1.x, r1.y, r1.z, r1.w};
+                const uint32_t a2[4] = {r2.x, r2.y, r2.z, r2.w}, a3[4] = {r3.x, r3.y, r3.z, r3.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int nb = 4 * q4 + k;
+                    const uint32_t b0 = hfma2_bits((prmt(a0[k], a1[k], vsel) & vmask) | 0x64006400u, vscale, vb[0]) & keep0;
+                    const uint32_t b1 = hfma2_bits((prmt(a2[k], a3[k], vsel) & vmask) | 0x64006400u, vscale, vb[1]) & keep1;
+                    mma16816(o[nb][0], o[nb][1], pad2, pad3, ahi[0], ahi[1], b0, b1);
+                    mma16816(o[nb][0], o[nb][1], pad2, pad3, alo[0], alo[1], b0, b1);
                 }
             }
         }
@@ -226,15 +314,17 @@ __global__ void __launch_bounds__(kAttnWarps * 32, QOQ_KV4_MINB) kv4_decode_attn
                      (uint32_t)hb, &full_bar[stg], policy);
         }
     }
-    // merge the 8 warps' partial softmax states
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-        if (l == 0) {
-            sm_m[w][j] = m[j];
-            sm_l[w][j] = lsum[j];
+    // merge the warps' partial softmax states (head gq of lanes 4gq..4gq+3)
+    if (gq < R) {
+        if (tq == 0) {
+            sm_m[w][gq] = m;
+            sm_l[w][gq] = lsum;
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) sm_acc[w][j][4 * l + i] = acc[j][i];
+        for (int nb = 0; nb < 16; ++nb) {
+            sm_acc[w][gq][8 * nb + 2 * tq] = o[nb][0];
+            sm_acc[w][gq][8 * nb + 2 * tq + 1] = o[nb][1];
+        }
     }
     cluster.sync();                                       // every CTA's warp states are in its smem
     if (rank == 0) {
