@@ -54,6 +54,9 @@ class QoQError(RuntimeError):
 def load() -> ctypes.CDLL:
     """Load libqoq_b200.so (raises if it was not built — no fallback)."""
     global _lib
+    if _lib is not None:
+        _sync_knobs(_lib)
+        return _lib
     with _lock:
         if _lib is not None:
             return _lib
@@ -85,14 +88,30 @@ def load() -> ctypes.CDLL:
             "qoq_kv4_decode_attention": (I, [P, P, P, P, I, I, I, I, I, I, P, P]),
             "qoq_linear_chain_workspace_bytes": (Z, [I, I, P]),
             "qoq_w4a8_linear_chain": (I, [I, I, P, P, Z, P]),
+            "qoq_debug_reload_knobs": (None, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
         if L.qoq_abi_version() != ABI_VERSION:
             raise ImportError("libqoq_b200.so ABI version mismatch; rebuild")
+        _sync_knobs(L)
         _lib = L
     return _lib
+
+
+_KNOB_VARS = ("QOQ_FORCE_MODE", "QOQ_BN_BIG", "QOQ_FORCE_CG", "QOQ_LINEAR_FUSED", "QOQ_CHAIN_SMAX", "QOQ_FQ_THREADS")
+_knob_seen = None
+
+
+def _sync_knobs(L):
+    """The library reads its QOQ_* test / tuning overrides once; re-read them when they changed here
+    (before any size query or launch, so both see the same plan)."""
+    global _knob_seen
+    cur = tuple(os.environ.get(k) for k in _KNOB_VARS)
+    if cur != _knob_seen:
+        L.qoq_debug_reload_knobs()
+        _knob_seen = cur
 
 
 def _check(fn: str, rc: int):

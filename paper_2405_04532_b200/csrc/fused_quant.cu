@@ -293,8 +293,7 @@ namespace {
 // Few rows (decode): 1024 threads per row (measured best at M = 64) so each thread's chain of loads is short; many rows
 // (prefill): K/32 threads (128..256) per row, many CTAs per SM overlapping their reduction latencies.
 int row_threads(int M, int K) {
-    if (const char* e = getenv("QOQ_FQ_THREADS")) {   // tuning override (tools only): 128..1024
-        const int t = atoi(e);
+    if (const int t = knobs().fq_threads) {            // tuning override (tools only): 128..1024
         if (t >= 128 && t <= 1024 && t % 32 == 0) return t;
     }
     if (M >= 2 * 148) return K >= 8192 ? 256 : 128;

@@ -10,6 +10,25 @@
 #include "../../include/qoq_b200.h"
 #include "qoq_internal.h"
 
+namespace qoq {
+
+static Knobs read_knobs() {
+    Knobs k;
+    auto get = [](const char* n, int def) { const char* e = getenv(n); return e ? atoi(e) : def; };
+    k.force_mode = get("QOQ_FORCE_MODE", -1);
+    k.bn_big = get("QOQ_BN_BIG", 0);
+    k.force_cg = get("QOQ_FORCE_CG", -1);
+    k.linear_fused = get("QOQ_LINEAR_FUSED", 0);
+    k.chain_smax = get("QOQ_CHAIN_SMAX", 0);
+    k.fq_threads = get("QOQ_FQ_THREADS", 0);
+    return k;
+}
+static Knobs g_knobs = read_knobs();   // process start (the library's load)
+const Knobs& knobs() { return g_knobs; }
+void reload_knobs() { g_knobs = read_knobs(); }
+
+}  // namespace qoq
+
 namespace {
 
 using namespace qoq;
@@ -106,8 +125,7 @@ int run_linear(const void* X, int ldx, int M, int N, int K, int group, const voi
     // Default: quantizer kernel + GEMM, PDL-chained (measured faster on B200 at every decode M: the
     // fused kernel's grid-wide handshake costs more than the kernel boundary it removes).
     // QOQ_LINEAR_FUSED=1 selects the one-kernel path for M <= kFuseMaxM.
-    const char* ff = getenv("QOQ_LINEAR_FUSED");
-    const bool fused = ff && atoi(ff) == 1;
+    const bool fused = knobs().linear_fused == 1;
     // the split-K region must be zero on entry; in a workspace shared by several shapes it may overlap
     // another shape's q_x, so the call clears it itself (mode-1 plans only: none at decode sizes)
     if (w.gemm_ws_bytes > 0 && cudaMemsetAsync(w.gemm_ws, 0, w.gemm_ws_bytes, st) != cudaSuccess) return QOQ_ERR_CUDA;
@@ -307,6 +325,9 @@ int qoq_pc_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed
                     static_cast<cudaStream_t>(stream), nullptr, z_w, true);
 }
 
+// Debug (not in the public header): re-read the QOQ_* test / tuning overrides from the environment.
+void qoq_debug_reload_knobs(void) { reload_knobs(); }
+
 // Debug (not in the public header): the fp16 GEMM with a per-CTA %globaltimer trace
 // (16 x u64 per CTA, grid <= #SMs) for pipeline timeline analysis (tools/trace_gemm.py).
 int qoq_debug_w4a8_gemm_trace(const int8_t* qx, const void* sx, const int32_t* tx, const void* packed,
@@ -426,8 +447,7 @@ static int run_chain(int M, int n, const qoq_linear_desc* desc, void* workspace,
     if ((rc = check_arch(&sms))) return rc;
     if (sms != num_sms_or_default()) return QOQ_ERR_CUDA;
     std::unique_ptr<ChainParams> pp(new ChainParams());   // ~16 KB of launch parameters (host heap)
-    const char* sc = getenv("QOQ_CHAIN_SMAX");              // tuning: cap on the k-splits per tile
-    const int chain_s_cap = sc ? atoi(sc) : 0;
+    const int chain_s_cap = knobs().chain_smax;             // tuning: cap on the k-splits per tile
     ChainParams& p = *pp;
     p.M = M;
     p.njobs = n;

@@ -32,6 +32,20 @@ struct GemmPlan {
 
 GemmPlan plan_gemm(int M, int N, int K, int num_sms);
 
+// Debug / test overrides of the planner and of the linear path, read from the environment ONCE (first use)
+// and re-read only by qoq_debug_reload_knobs() (the Python binding calls it when a QOQ_* variable it
+// forwards changes, so pytest's monkeypatch works). Production launches never call getenv.
+struct Knobs {
+    int force_mode = -1;     // QOQ_FORCE_MODE: 0 / 1 / 2
+    int bn_big = 0;          // QOQ_BN_BIG: 128 / 192 / 256 (prefill token tile)
+    int force_cg = -1;       // QOQ_FORCE_CG: 2 = CTA pairs (slower, opt-in)
+    int linear_fused = 0;    // QOQ_LINEAR_FUSED: 1 = the one-kernel linear for M <= 64 (slower, opt-in)
+    int chain_smax = 0;      // QOQ_CHAIN_SMAX: cap on the decode chain's k-splits per tile (tuning)
+    int fq_threads = 0;      // QOQ_FQ_THREADS: fused quantizer threads per row (tuning)
+};
+const Knobs& knobs();
+void reload_knobs();
+
 struct GemmArgs {
     const int8_t* qx;
     const void* sx;

@@ -166,6 +166,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef QOQ_PDL_EARLY
 #define QOQ_PDL_EARLY 0
 #endif
+#ifndef QOQ_W_L2_PREFETCH
+#define QOQ_W_L2_PREFETCH 0   // bulk L2 prefetch of each decode segment's weights (A/B knob)
+#endif
 #ifndef QOQ_W_PREFILL
 #define QOQ_W_PREFILL 1   // W-ring stages issued before the setup barrier (each issue costs ~250 cycles)
 #endif
@@ -263,6 +266,18 @@ struct WProducer {
         if (live) tile_coords(p, tile, nu, mt);
         nt = nu * cg + rank;
         pol = policy_evict_first();   // each weight byte is read once
+        if (live && threadIdx.x == 0) prefetch_segment(p, s0);   // the weight producer thread
+    }
+    // Decode (one token tile): ask L2 for the whole segment's packed weights up front, so the HBM reads run
+    // at full parallelism and the SMEM ring's bulk copies hit L2 (one SM pulls only ~27 B/cycle from HBM
+    // through its own copies; a 32-tile o_proj would otherwise stream at 32 SMs' ingress).
+    __device__ void prefetch_segment(const KParams& p, int s0) {
+#if QOQ_W_L2_PREFETCH
+        if (p.MT != 1) return;
+        const uint8_t* a = p.packed + ((size_t)nt * p.KT + 2 * s0) * C::kTB;
+        const uint8_t* e = p.packed + ((size_t)nt * p.KT + (2 * s1 < p.KT ? 2 * s1 : p.KT)) * C::kTB;
+        for (; a < e; a += 65536) prefetch_l2_bulk(a, (uint32_t)((e - a) < 65536 ? (e - a) : 65536));
+#endif
     }
     __device__ bool issue(const KParams& p, uint8_t* smem, uint64_t* wfull, uint64_t* wfree) {
         if (!live) return false;
@@ -284,6 +299,7 @@ struct WProducer {
                 int nu, mt;
                 tile_coords(p, tile, nu, mt);
                 nt = nu * cg + rank;
+                prefetch_segment(p, s0);
             }
         }
         return true;
@@ -1028,8 +1044,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
         // save). Relative per-token costs measured on B200 (tools/prefill_ab.sh): BN = 128 expands
         // each weight tile for half as many tokens (~1.2x); BN = 256 runs its epilogue without
         // overlap (~1.2x at K = 4096, shrinking with K). QOQ_BN_BIG=128/192/256 forces.
-        const char* fb = getenv("QOQ_BN_BIG");
-        const int force = fb ? atoi(fb) : 0;
+        const int force = knobs().bn_big;
         const int cand[3] = {128, 192, 256};
         const double eff[3] = {1.2, 1.0, 1.0 + 0.2 * 4096.0 / K};
         double best = 1e300;
@@ -1063,8 +1078,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     //    down_proj M=64) edges out stream-K through the L2 workspace (mode 1, 14.6 us).
     //  * BN >= 128 with T < #SMs: stream-K (mode 1).
     // QOQ_FORCE_MODE=0/1/2 overrides (debug / tests).
-    const char* fm = getenv("QOQ_FORCE_MODE");
-    const int force = fm ? atoi(fm) : -1;
+    const int force = knobs().force_mode;
     int want;
     if (force >= 0 && force <= 2) want = force;
     else if (p.T >= num_sms) want = 0;
@@ -1100,8 +1114,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     }
     // CTA pairs (cta_group::2) for modes 0 / 1 when the 128-row tiles pair up. Work units become
     // tile pairs: T = units, G = pairs (the grid is 2G CTAs in clusters of 2).
-    const char* fp = getenv("QOQ_FORCE_CG");
-    const int force_cg = fp ? atoi(fp) : -1;
+    const int force_cg = knobs().force_cg;
     const bool pair_ok = p.mode != 2 && p.NT % 2 == 0 && p.BN >= 32;
     // Opt-in for now (QOQ_FORCE_CG=2): bit-exact, but on B200 two of the four dequant warps' tcgen05.st
     // stall for thousands of cycles while the pair's cta_group::2 MMAs run (tools/trace_gemm.py), so
