@@ -12,6 +12,7 @@
 // The dequantization (q − z)·s is folded out of both contractions: the tensor cores multiply exact fp16
 // integers (q − z) and the scales are applied to the fp32 results (QK) or to the probabilities (PV).
 #include <cooperative_groups.h>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cstdint>
 
@@ -88,11 +89,11 @@ __global__ void __launch_bounds__(64) kv4_append_kernel(const __half* __restrict
 // (padded to 16), so both contractions run as mma.sync.m16n8k16 (fp16 inputs, fp32 accumulation):
 //   S[h][t] = Σ_d q[h][d] · (c_K[t][d] − z_K[t])           (QK: A = q, B = integer codes − zero point)
 //   score    = S · s_K[t] · log2(e)/√D                       (the scale folded out of the dot product)
-//   O[h][d] += Σ_t (p[h][t] · s_V[t]) · (c_V[t][d] − z_V[t]) (PV: A = p·s_V split hi + lo in fp16,
-//                                                             B = integer codes − zero point)
-// Every fp16 input is exact: q as given, c − z ∈ [−15, 15], and p·s_V carried as two fp16 terms (≈ 22
-// significant bits), so the only roundings are the fp32 accumulations — the error model of
-// tests/kv4_tol.py. The QK accumulator fragment of two 8-token blocks IS the PV A fragment (heads ×
+//   O[h][d] += Σ_t (p[h][t] · s_V[t]) · (c_V[t][d] − z_V[t]) (PV in bf16: A = p·s_V split into three bf16
+//                                                             terms, B = integer codes − zero point)
+// Every MMA input is exact: q as given (fp16), c − z ∈ [−15, 15], and p·s_V carried as three bf16 terms
+// (≈ 24 significant bits over fp32's exponent range), so the only roundings are the fp32 accumulations —
+// the error model of tests/kv4_tol.py. The QK accumulator fragment of two 8-token blocks IS the PV A fragment (heads ×
 // tokens), so scores never leave registers. Online softmax in base 2 per head (a quad of lanes).
 
 // mma.sync m16n8k16, row.col, f16 x f16 -> f32, accumulating rows gq (d0, d1) in place. A's rows gq + 8
@@ -106,6 +107,16 @@ __device__ __forceinline__ void mma16816(float& d0, float& d1, float& p2, float&
         : "+f"(d0), "+f"(d1), "+f"(p2), "+f"(p3)
         : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
+
+// The same MMA with bf16 operands (PV: the probabilities need fp32's exponent range, see below).
+__device__ __forceinline__ void mma16816_bf16(float& d0, float& d1, float& p2, float& p3, uint32_t a0, uint32_t a2,
+                                              uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d0), "+f"(d1), "+f"(p2), "+f"(p3)
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t bf2bits(__nv_bfloat162 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
 // Codes to exact fp16 (c − z) with 3 instructions per half2: PRMT places the code bytes under 0x64 high
 // bytes, LOP3 keeps one nibble per half (0x6400 | c = 1024 + c, or 0x6400 | 16c = 1024 + 16c), and one
@@ -176,12 +187,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32, QOQ_KV4_MINB) kv4_decode_attn
     }
     const uint32_t ksel = 0x4040u | (0x0101u * (uint32_t)tq);   // PRMT: bytes (w.tq, 0x64, w.tq, 0x64)
     const uint32_t kscale = 0x2C003C00u;                   // half2 (1, 1/16)
-    // V: nibble (gq & 1) of byte (gq >> 1) of word nb, for two tokens: PRMT (w0.byte, -, w1.byte, -), keep the
-    // nibble, OR in the 0x64 high bytes
+    // V (bf16): nibble (gq & 1) of byte (gq >> 1) of word nb, for two tokens: PRMT (w0.byte, -, w1.byte, -),
+    // shift the nibble down, OR in the bf16 128.0 exponent (0x4300 | c = 128 + c), subtract 128 + z
     const uint32_t vsel = (uint32_t)(gq >> 1) | ((4u + (gq >> 1)) << 8);
-    const uint32_t vmask = (gq & 1) ? 0x00F000F0u : 0x000F000Fu;
-    const uint32_t vscale = (gq & 1) ? 0x2C002C00u : 0x3C003C00u;   // (1/16, 1/16) or (1, 1)
-    const float vbase = (gq & 1) ? 64.0f : 1024.0f;
+    const uint32_t vshift = 4u * (uint32_t)(gq & 1);
     for (int n = 0; n < my_pages; ++n) {
         const int stg = n % kKvStages;
         mbar_wait(&full_bar[stg], (uint32_t)((n / kKvStages) & 1));
@@ -255,8 +264,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32, QOQ_KV4_MINB) kv4_decode_attn
                     o[nb][1] *= corr;
                 }
             }
-            // ---- PV: A = p · s_V (hi + lo fp16) for tokens (2tq, 2tq+1) and (8 + 2tq, 9 + 2tq)
-            uint32_t ahi[2], alo[2];
+            // ---- PV: A = p · s_V for tokens (2tq, 2tq+1) and (8 + 2tq, 9 + 2tq) as THREE bf16 terms (≈ 24
+            // significant bits with fp32's exponent range: a tiny p · s_V would lose its precision in fp16's
+            // subnormals), B = V codes − z (exact small integers in bf16)
+            uint32_t ap[3][2];
 #pragma unroll
             for (int nbt = 0; nbt < 2; ++nbt) {
                 float f[2];
@@ -266,10 +277,14 @@ __global__ void __launch_bounds__(kAttnWarps * 32, QOQ_KV4_MINB) kv4_decode_attn
                     const float sv = __half2float(__ushort_as_half((unsigned short)(par[P + o0 + tt] & 0xFFFFu)));
                     f[u] = pv[nbt][u] * sv;
                 }
-                const __half2 hi = __floats2half2_rn(f[0], f[1]);
-                const float2 hf = __half22float2(hi);
-                ahi[nbt] = h2bits(hi);
-                alo[nbt] = h2bits(__floats2half2_rn(f[0] - hf.x, f[1] - hf.y));
+                const __nv_bfloat162 h1 = __floats2bfloat162_rn(f[0], f[1]);
+                const float2 g1 = __bfloat1622float2(h1);
+                const float r0 = f[0] - g1.x, r1 = f[1] - g1.y;
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(r0, r1);
+                const float2 g2 = __bfloat1622float2(h2);
+                ap[0][nbt] = bf2bits(h1);
+                ap[1][nbt] = bf2bits(h2);
+                ap[2][nbt] = bf2bits(__floats2bfloat162_rn(r0 - g2.x, r1 - g2.y));
             }
             // B fragments: V codes of tokens 2tq, 2tq+1 (b0) and 8+2tq, 9+2tq (b1) at d = 8nb + gq
             const uint4* vr[4];
@@ -278,13 +293,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32, QOQ_KV4_MINB) kv4_decode_attn
                 const int tt = (i < 2 ? 0 : 8) + 2 * tq + (i & 1);
                 vr[i] = reinterpret_cast<const uint4*>(base + (size_t)(P + o0 + tt) * (kKvD / 2));
             }
-            uint32_t vb[2];                                // −(base + z) of the two tokens of each pair
+            __nv_bfloat162 vb[2];                          // 128 + z of the two tokens of each pair
 #pragma unroll
             for (int pr = 0; pr < 2; ++pr) {
                 const int t0 = 8 * pr + 2 * tq;
-                const __half z0 = __ushort_as_half((unsigned short)(par[P + o0 + t0] >> 16));
-                const __half z1 = __ushort_as_half((unsigned short)(par[P + o0 + t0 + 1] >> 16));
-                vb[pr] = h2bits(__halves2half2(__hneg(__hadd(__float2half(vbase), z0)), __hneg(__hadd(__float2half(vbase), z1))));
+                const float z0 = __half2float(__ushort_as_half((unsigned short)(par[P + o0 + t0] >> 16)));
+                const float z1 = __half2float(__ushort_as_half((unsigned short)(par[P + o0 + t0 + 1] >> 16)));
+                vb[pr] = __floats2bfloat162_rn(128.0f + z0, 128.0f + z1);
             }
             // masked tokens (past the sequence end, only in its last chunk) take p = 0 and code = z (no
             // NaN / Inf from never-written page bytes)
@@ -299,10 +314,12 @@ __global__ void __launch_bounds__(kAttnWarps * 32, QOQ_KV4_MINB) kv4_decode_attn
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int nb = 4 * q4 + k;
-                    const uint32_t b0 = hfma2_bits((prmt(a0[k], a1[k], vsel) & vmask) | 0x64006400u, vscale, vb[0]) & keep0;
-                    const uint32_t b1 = hfma2_bits((prmt(a2[k], a3[k], vsel) & vmask) | 0x64006400u, vscale, vb[1]) & keep1;
-                    mma16816(o[nb][0], o[nb][1], pad2, pad3, ahi[0], ahi[1], b0, b1);
-                    mma16816(o[nb][0], o[nb][1], pad2, pad3, alo[0], alo[1], b0, b1);
+                    uint32_t x0 = ((prmt(a0[k], a1[k], vsel) >> vshift) & 0x000F000Fu) | 0x43004300u;
+                    uint32_t x1 = ((prmt(a2[k], a3[k], vsel) >> vshift) & 0x000F000Fu) | 0x43004300u;
+                    const uint32_t b0 = bf2bits(__hsub2(*reinterpret_cast<const __nv_bfloat162*>(&x0), vb[0])) & keep0;
+                    const uint32_t b1 = bf2bits(__hsub2(*reinterpret_cast<const __nv_bfloat162*>(&x1), vb[1])) & keep1;
+#pragma unroll
+                    for (int e = 0; e < 3; ++e) mma16816_bf16(o[nb][0], o[nb][1], pad2, pad3, ap[e][0], ap[e][1], b0, b1);
                 }
             }
         }

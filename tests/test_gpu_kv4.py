@@ -136,3 +136,22 @@ def test_kv4_attention_page_sizes(gpu_lib, page):
     """Other page sizes: 32 (the smallest allowed) and 256 (the largest: 3 staged pages of 34.8 KB in
     shared memory, past the default 48 KB)."""
     check_attention(gpu_lib, [1, page - 1, page, page + 1, 3 * page + 5], 32, 8, seed=page, P=page)
+
+
+def test_kv4_attention_peaked_outlier_data(gpu_lib):
+    """The smoke test's data: Q, K and V with 4 input channels scaled x20 (synth.activations_fp16), so the
+    softmax is sharply peaked and most p·s_V are far below fp16's normal range — the PV operand must keep
+    its relative precision there (bf16 terms) for the derived tolerance to hold."""
+    T, H, H_kv, P_ = 70, 8, 2, 64
+    Kx = synth.activations_fp16(T * H_kv, D, seed=2).reshape(T, H_kv, D)
+    Vx = synth.activations_fp16(T * H_kv, D, seed=3).reshape(T, H_kv, D)
+    bt = np.array([[1, 0]], np.int32)
+    pages, deq = oracle_cache([Kx], [Vx], bt, 2, P_)
+    Q = synth.activations_fp16(H, D, seed=4).reshape(1, H, D)
+    O = gpu_lib.kv4_decode_attention(to_dev(Q), to_dev(pages), to_dev(bt), to_dev(np.array([T], np.int32)), H_kv, P_)
+    torch.cuda.synchronize()
+    Kh, Vh = deq[0]
+    ref = oracle.attention_f64(Q[0], Kh, Vh)
+    err = np.abs(O.cpu().numpy()[0].astype(np.float64) - ref)
+    tol = kv4_tolerance(Q[0], Kh, Vh, ref)
+    assert np.all(err <= tol), f"max err/tol {(err / tol).max()}"
