@@ -1,7 +1,11 @@
 """Derived per-element tolerance for KV4 decode attention (reading Q29).
 
 The GPU kernel attends over the SAME dequantized cache K̂, V̂ as the oracle (pages are byte-exact and
-(q - z)·s is exact in fp32), so the only differences are fp32 arithmetic and the fp16 output:
+(q - z)·s is exact in fp32), so the only differences are fp32 arithmetic and the fp16 output. Since
+round 2 the kernel runs both products on tensor cores (mma.sync m16n8k16, fp32 accumulators): QK takes
+fp16 q times the exact integers c - z and applies s_K·log2e/√D to the accumulator; PV takes p·s_V as a
+sum of three bf16 terms (24 significant bits, i.e. the fp32 value up to ≤ u relative) times c - z. The
+products are exact and every rounding is an fp32 accumulation, which the terms below bound:
 
   * output rounding to fp16:                       ≤ 2^-11 |o|  (+ 2^-25 absolute in the subnormal range)
   * score s_t = Σ_d q_d k̂_td / √D in fp32:        |δs_t| ≤ (D + 2)·u·S_t,  S_t = Σ_d |q_d k̂_td| / √D,
