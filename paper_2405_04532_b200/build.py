@@ -4,6 +4,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -32,14 +33,17 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     out = lib_path(variant)
     if not force and not variant and not _stale():
         return LIB
-    objs = []
+    objs, cmds = [], []
     for s in SOURCES:
         o = os.path.join(CSRC, s.replace(".cu", f"{variant}.o"))
-        cmd = [NVCC, *FLAGS, *(extra or []), "-c", os.path.join(CSRC, s), "-o", o]
+        cmds.append([NVCC, *FLAGS, *(extra or []), "-c", os.path.join(CSRC, s), "-o", o])
         if verbose:
-            print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+            print(" ".join(cmds[-1]), file=sys.stderr)
         objs.append(o)
+    # translation units compile in parallel (the GEMM and chain files dominate)
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+            f.result()
     tmp = out + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
                            "-o", tmp, *objs, "-lcuda" if False else "-ldl"])

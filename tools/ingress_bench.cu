@@ -8,12 +8,12 @@
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-constexpr int kStep = 16896, kRing = 6, kIters = 400;
+constexpr int kStep = 16896, kRingMax = 12, kIters = 400;
 
-__global__ void __launch_bounds__(160, 1) ingress(const uint8_t* w, size_t per, int use_tma, int use_lsu,
+__global__ void __launch_bounds__(160, 1) ingress(const uint8_t* w, size_t per, int use_tma, int use_lsu, int kRing,
                                                   long long* cyc, long long* bytes) {
     extern __shared__ __align__(1024) uint8_t sm[];
-    __shared__ __align__(8) uint64_t bar[kRing];
+    __shared__ __align__(8) uint64_t bar[kRingMax];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint8_t* base = w + per * blockIdx.x;
     if (threadIdx.x == 0) {
@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(160, 1) ingress(const uint8_t* w, size_t per, 
     const long long t0 = clock64();
     long long moved = 0;
     if (warp == 0 && lane == 0 && use_tma) {
-        uint32_t ph[kRing] = {0, 0, 0, 0, 0, 0};
+        uint32_t ph[kRingMax] = {0};
         size_t off = 0;
         for (int it = 0; it < kIters; ++it) {
             const int i = it % kRing;
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(160, 1) ingress(const uint8_t* w, size_t per, 
     }
     if (warp >= 1 && use_lsu) {   // 4 warps of cp.async 16-byte copies into a separate region, 4 groups in flight
         const int t = threadIdx.x - 32;   // 0..127
-        uint8_t* dst = sm + kRing * 17408;
+        uint8_t* dst = sm + 6 * 17408;
         const uint8_t* src = base + per / 2;
         for (int it = 0; it < kIters; ++it) {
             for (int c = 0; c < kStep / (128 * 16); ++c) {   // 8 x 2 KB = 16 KB per iteration
@@ -79,22 +79,22 @@ int main() {
     cudaMemset(w, 1, per * 148);
     cudaMalloc(&cyc, 8 * 148);
     cudaMalloc(&bytes, 8 * 148);
-    const int smem = kRing * 17408 + 4 * 16384;
+    const int smem = kRingMax * 17408 + 8192;
     cudaFuncSetAttribute(ingress, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const char* names[3] = {"TMA bulk", "cp.async", "both"};
-    for (int G : {32, 148}) {
-        for (int mode = 0; mode < 3; ++mode) {
+    for (int G : {32, 148}) for (int ring : {2, 4, 6, 9, 12}) {
+        for (int mode = 0; mode < 1; ++mode) {
             long long hc[148], hb[148];
             for (int rep = 0; rep < 2; ++rep) {
                 cudaMemset(bytes, 0, 8 * 148);
-                ingress<<<G, 160, smem>>>(w, per, mode != 1, mode != 0, cyc, bytes);
+                ingress<<<G, 160, smem>>>(w, per, mode != 1, mode != 0, ring, cyc, bytes);
                 cudaDeviceSynchronize();
             }
             cudaMemcpy(hc, cyc, 8 * G, cudaMemcpyDeviceToHost);
             cudaMemcpy(hb, bytes, 8 * G, cudaMemcpyDeviceToHost);
             double s = 0;
             for (int b = 0; b < G; ++b) s += (double)hb[b] / hc[b];
-            printf("G=%3d %-9s: %6.1f B/cycle per SM (%.2f TB/s at 1.965 GHz)\n", G, names[mode], s / G, s * 1.965e9 / 1e12);
+            printf("ring=%2d G=%3d %-9s: %6.1f B/cycle per SM (%.2f TB/s at 1.965 GHz)\n", ring, G, names[mode], s / G, s * 1.965e9 / 1e12);
         }
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
