@@ -426,3 +426,15 @@ def attention_f64(Q: np.ndarray, Khat: np.ndarray, Vhat: np.ndarray) -> np.ndarr
                                       _p(np.ascontiguousarray(Vhat, np.float64)), T, H, H_kv, D, _p(O)),
            "attention_f64")
     return O
+
+
+def tp_reduce_rank_order(partials) -> np.ndarray:
+    """Row-parallel TP reduction (north_star: "o_proj/down are row-sharded over K, finished by an ... allreduce
+    of the FP16 partials"; reading Q17 for the per-rank partial, Q32 for the order): the fp16 partials Y_0 ..
+    Y_{R-1} of the ranks, widened to fp32 and summed in RANK ORDER, one IEEE fp32 addition at a time, then
+    rounded once to fp16 (RNE). The paper is single-GPU; the order is this build's reading."""
+    acc = None
+    for y in partials:
+        f = np.asarray(y, dtype=np.float16).astype(np.float32)
+        acc = f.copy() if acc is None else (acc + f).astype(np.float32)
+    return acc.astype(np.float16)
