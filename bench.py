@@ -295,6 +295,8 @@ def main():
                     help="skip the per-channel W4A8 (NEXT-1) decode step measurement")
     ap.add_argument("--unfused-gate-up", action="store_true", help="run gate and up as two GEMMs")
     ap.add_argument("--no-chain", action="store_true", help="skip the persistent decode chain measurement")
+    ap.add_argument("--no-tp-fused", action="store_true",
+                    help="skip the fused TP reduction leg (NEXT-3, qoq_w4a8_gemm_allreduce)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the decode M sweep (C2: M = 1 .. 256)")
     ap.add_argument("--fused-quant", action="store_true",
                     help="qoq_w4a8_linear per linear: per-token quantization fused into the GEMM prologue "
@@ -365,10 +367,30 @@ def main():
     if fused_quant:
         os.environ["QOQ_LINEAR_FUSED"] = "1"   # w4a8_linear's opt-in one-kernel path (read per call)
 
-    def make_linear(gemm_only, counter):
+    # NEXT-3: the fused TP reduction of the row-parallel layers (qoq_w4a8_gemm_allreduce). Its buffers are
+    # symmetric memory over the TP group (N > 1) or local (N = 1: the protocol's own cost, one partial)
+    tp_comm, tp_comm_err = None, None
+    if not args.no_tp_fused:
+        n_cap = max(Nr for _, Nr, _, kind, _ in shapes if kind == "row")
+        try:
+            tp_comm = (parallel.fused_tp_comm(qoq, dist.group.WORLD, M, n_cap, dev) if world > 1
+                       else qoq.TpComm.local(M, n_cap, dev))
+        except Exception as e:   # reported in the line; the NCCL step is the measured default
+            tp_comm_err = f"{type(e).__name__}: {e}"
+
+    def make_linear(gemm_only, counter, fused_rows=False):
         def linear(X_r, shard, entry):
             name, Nr, Kr, N, K, kind, qg = entry
             p, s0 = shard
+            if fused_rows and kind == "row":
+                if not gemm_only and qg not in counter[1]:
+                    qoq.quantize_activations_per_token(X_r, out=quant_out[qg], stream=stream)
+                    counter[1].add(qg)
+                    counter[0] += 1
+                qx, sx, tx = quant_out[qg]
+                qoq.w4a8_gemm_allreduce(qx, sx, tx, p, s0, Nr, tp_comm, out=Ybuf[name], stream=stream)
+                counter[0] += 1
+                return Ybuf[name]
             if fused_quant and not gemm_only:
                 # the public linear call: per-token quantization fused into the GEMM (M <= 64)
                 Xc = X_r if X_r.is_contiguous() else X_r.contiguous()
@@ -385,14 +407,16 @@ def main():
             return Ybuf[name]
         return linear
 
-    def run_step(gemm_only=False, collective=True):
+    def run_step(gemm_only=False, collective=True, fused_rows=False):
         """One decode step: every layer through parallel.tp_decode_layer (the code path the gloo tests
-        drive), the all-reduces of the row-parallel partials on `stream`."""
+        drive), the all-reduces of the row-parallel partials on `stream` — or, fused_rows, reduced inside the
+        row-parallel GEMMs (NEXT-3)."""
         n_launch = 0
         for l in range(layers):
             counter = [0, set()]
             ar = (lambda Y: dist.all_reduce(Y)) if (world > 1 and collective and not gemm_only) else (lambda Y: None)
-            parallel.tp_decode_layer(X, packed[l], plan, make_linear(gemm_only, counter), ar, rank, world)
+            parallel.tp_decode_layer(X, packed[l], plan, make_linear(gemm_only, counter, fused_rows), ar, rank, world,
+                                     fused_rows=fused_rows)
             n_launch += counter[0]
         return n_launch
 
@@ -443,6 +467,47 @@ def main():
         ms_gemm = timed(g_gemm, max(10, args.steps // 2), 2)
         ms_nocoll = timed(g_nocoll, max(10, args.steps // 2), 2) / max(10, args.steps // 2) if g_nocoll else None
 
+    # ---- NEXT-3: the same step with the row-parallel reductions fused into the GEMM epilogues. One eager step
+    # first: a peer wait that timed out (status) or outputs outside the propagated tolerance of the NCCL step
+    # disable the timed leg instead of timing a broken protocol. N = 1: the protocol's own cost per launch on
+    # the TP = 8 row-parallel shard shapes (the one-partial reduction against the plain GEMM)
+    tp_fused = None
+    if tp_comm is not None and world == 1:
+        try:
+            tp_fused = tp_fused_overhead(qoq, torch, args, dev, stream, timed)
+        except Exception as e:
+            tp_fused = {"unavailable": f"{type(e).__name__}: {e}"}
+    elif tp_comm is not None:
+        try:
+            with torch.cuda.stream(stream):
+                run_step()
+                ref_rows = {n: Ybuf[n].clone() for n, _, _, kind, _ in shapes if kind == "row"}
+                run_step(fused_rows=True)
+            stream.synchronize()
+            if world > 1:
+                dist.barrier()
+            st = tp_comm.status()
+            diff = max(float((Ybuf[n].float() - ref_rows[n].float()).abs().max()) for n in ref_rows)
+            scale = max(float(ref_rows[n].float().abs().max()) for n in ref_rows)
+            ok = st == 0 and diff <= 4e-3 * scale + 2e-3 * world
+            tp_fused = {"status": st, "max_abs_diff_vs_nccl_step": diff, "ok": ok}
+            if ok:
+                g_fused = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_fused, stream=stream):
+                    run_step(fused_rows=True)
+                with torch.cuda.stream(stream):
+                    nst = max(10, args.steps // 2)
+                    ms_f = timed(g_fused, nst, 2) / nst
+                tp_fused.update({"ms_per_step": ms_f, "GBps": step_work(args.model, M, layers, world, fused)[0]
+                                 / (ms_f * 1e-3) / 1e9, "status_after": tp_comm.status()})
+        except Exception as e:
+            tp_fused = {"unavailable": f"{type(e).__name__}: {e}"}
+        tp_fused["what"] = ("decode step with the row-parallel all-reduces fused into the o / down GEMM epilogues "
+                            "(qoq_w4a8_gemm_allreduce: fp16 partial tiles pushed to every rank's symmetric buffer, "
+                            "reduced in rank order, NEXT-3)")
+    elif tp_comm_err:
+        tp_fused = {"unavailable": tp_comm_err}
+
     ms_step = ms_total / args.steps
     step_bytes, step_ops = step_work(args.model, M, layers, world, fused)
     value = step_bytes / (ms_step * 1e-3) / 1e9
@@ -488,6 +553,8 @@ def main():
                       "t_roofline_1gpu_ms": t_roof,
                       "collective": "torch.distributed.all_reduce (NCCL) of the fp16 row-parallel partials"}
 
+    if tp_fused is not None:
+        line["tp_fused"] = tp_fused
     if world == 1 and not args.no_chain and M <= 128:
         line["decode_chain"] = chain_measure(qoq, torch, args, plan, packed, layers, dev, stream, X, step_bytes, timed)
     if world == 1 and not args.no_sweep:
@@ -615,6 +682,50 @@ def e2e_measure(qoq, torch, dist, args, shapes, packed, layers, world, dev, stre
             "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": steps, "streams": nstreams,
             "api": "qoq_linear_host (C ABI, pinned host X/Y) per GEMM, calls alternating over "
                    f"{nstreams} streams, the step captured as one CUDA graph"}
+
+
+def tp_fused_overhead(qoq, torch, args, dev, stream, timed, world_tp=8, reps=16):
+    """NEXT-3 at N = 1: per-launch time of qoq_w4a8_gemm_allreduce with a one-rank comm (push, flag, wait and
+    rank-order reduction all local) against qoq_w4a8_gemm on the row-parallel shard shapes of TP = world_tp
+    (o: K / world_tp, down: I / world_tp), graphs of `reps` distinct weights each."""
+    M = args.M
+    gen = torch.Generator(device=dev)
+    out = {}
+    for name, N, K, kind in model_shapes(args.model, True):
+        if kind != "row":
+            continue
+        Kr = K // world_tp
+        packs = []
+        for i in range(reps):
+            gen.manual_seed(9000 + i)
+            packs.append(qoq.quantize_weights(synth.device_weights_fp16(N, Kr, gen, dev), stream=stream))
+        qx, sx, tx = qoq.quantize_activations_per_token(synth.device_activations_fp16(M, Kr, gen, dev), stream=stream)
+        Y = torch.empty(M, N, dtype=torch.float16, device=dev)
+        comm = qoq.TpComm.local(M, N, dev)
+        ws = qoq.Workspace(dev)
+        ws.get(qoq.gemm_workspace_bytes(M, N, Kr))
+        res = {}
+        for leg in ("gemm", "fused"):
+            def run():
+                for p, s0 in packs:
+                    if leg == "gemm":
+                        qoq.w4a8_gemm(qx, sx, tx, p, s0, N, out=Y, workspace=ws, stream=stream)
+                    else:
+                        qoq.w4a8_gemm_allreduce(qx, sx, tx, p, s0, N, comm, out=Y, stream=stream)
+            with torch.cuda.stream(stream):
+                run()
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                run()
+            with torch.cuda.stream(stream):
+                res[leg + "_us"] = timed(g, 20, 3) / 20 / reps * 1e3
+        res["status"] = comm.status()
+        out[f"{name}_N{N}_K{Kr}"] = res
+    return {"per_launch": out, "M": M, "tp_shard_of": world_tp,
+            "what": "N = 1: qoq_w4a8_gemm_allreduce with a one-rank comm (the fused reduction's own cost: local "
+                    "flag-in-data push and rank-order reduce) vs qoq_w4a8_gemm, on the TP = 8 "
+                    "row-parallel shard shapes; the cross-GPU leg runs under torchrun (N > 1)"}
 
 
 def chain_measure(qoq, torch, args, plan, packed, layers, dev, stream, X, step_bytes, timed):

@@ -40,7 +40,7 @@ typedef enum {
 const char* qoq_status_string(int status);
 /* ABI version of this header (incremented on any signature or layout change). */
 int qoq_abi_version(void);
-#define QOQ_ABI_VERSION 6
+#define QOQ_ABI_VERSION 7
 
 /* ----------------------------------------------------------------------------------------------
  * Packed weight layout (frozen). The B200 form of "store the weights in the order
@@ -244,12 +244,52 @@ int qoq_kv4_decode_attention(const void* Q_fp16, const void* pages, const int32_
                              const int32_t* seq_lens, int B, int H, int H_kv, int D, int page_size, int max_pages,
                              void* O_fp16, void* stream);
 
+/* ----------------------------------------------------------------------------------------------
+ * Fused tensor-parallel reduction of a row-parallel linear (NEXT-3; ABI v7). The north_star's
+ * Megatron split: o_proj / down are row-sharded over K, and Y = Σ_r Y_r over the TP ranks, where rank r's
+ * partial is Y_r = fp16(acc_r · s_x^r · s0) of its K shard (reading Q17; the paper itself is single-GPU,
+ * P:754). qoq_w4a8_gemm_allreduce computes Y_r tile by tile (whole 128-row tiles) and, in the same
+ * kernel's epilogue, PUSHES each fp16 partial tile into slot `rank` of every rank's receive buffer (peer
+ * stores over NVLink), then writes
+ *     Y[m][n] = fp16( Σ_{q = 0 .. world-1} fp32(Y_q[m][n]) )      summed in rank order (reading Q32)
+ * from its own buffer as the peers' words arrive, so every rank ends with identical bits and the transfer
+ * of one tile overlaps the math of the others. Slots hold 8-byte words {two fp16, uint32 flag}; a word is
+ * valid when its flag equals this call's number (no fences, no counters).
+ *
+ * qoq_tp_comm (host struct, read during the call; every pointer is a DEVICE pointer):
+ *   recv[q] (q < world) rank q's receive buffer, a device pointer valid on this GPU (peer-mapped, e.g.
+ *          symmetric memory): qoq_tp_recv_bytes(world, m_cap, n_cap) bytes ([2 parities][world slots][m_cap]
+ *          [n_cap / 2] words), 16-byte aligned, zero-initialized once; entries >= world are ignored;
+ *   gen, done  one uint32 each (this rank's call counter and CTA exit counter), zero-initialized once;
+ *   status one int32, zero-initialized; set to 1 if a wait for a peer exceeded 2 s (the call then gives up
+ *          and Y is unspecified) — check it after synchronizing;
+ *   rank, world (1 .. QOQ_TP_MAX_WORLD), m_cap >= M, n_cap >= N (n_cap % 128 == 0).
+ * Every rank must issue the same sequence of qoq_w4a8_gemm_allreduce calls (same M, N) on its own GPU with
+ * the same comm layout; the buffers alternate by call parity, so no barrier is needed between calls.
+ * world == 1 is valid (the push and the wait are local; Y equals qoq_w4a8_gemm bit for bit).
+ * Other arguments and errors as qoq_w4a8_gemm (tx nullable); comm / capacity violations ->
+ * QOQ_ERR_INVALID_ARG. Launches 1 kernel. Ownership: the caller allocates and shares the buffers; the
+ * library only reads and writes them inside the kernel. */
+#define QOQ_TP_MAX_WORLD 8
+typedef struct {
+    void* recv[QOQ_TP_MAX_WORLD];
+    uint32_t* gen;
+    uint32_t* done;
+    int32_t* status;
+    int rank, world;
+    int m_cap, n_cap;
+} qoq_tp_comm;
+size_t qoq_tp_recv_bytes(int world, int m_cap, int n_cap);
+int qoq_w4a8_gemm_allreduce(const int8_t* qx, const void* sx_fp16, const int32_t* tx, const void* packed,
+                            const void* s0_fp16, int M, int N, int K, int group, void* Y_fp16, int ldy,
+                            const qoq_tp_comm* comm, void* stream);
+
 /* Kernels launched per successful call (launch accounting for benchmarks):
  * quantize_weights 2, quantize_activations_per_token 1, rmsnorm_quantize 1, silu_mul_quantize 1,
  * kv4_append 1, kv4_decode_attention 1, w4a8_gemm 1, w4a8_gemm_i32 1,
  * pc_quantize_weights 2, pc_w4a8_gemm 1, pc_w4a8_gemm_i32 1,
  * w4a8_linear 2 (1 when fused: QOQ_LINEAR_FUSED=1 and M <= 64), linear_host as w4a8_linear,
- * w4a8_linear_chain 1 (for the whole chain)
+ * w4a8_linear_chain 1 (for the whole chain), w4a8_gemm_allreduce 1
  * (plus 2 async copies). */
 
 #ifdef __cplusplus

@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libqoq_b200.so" if not os.environ.get("QOQ_LIB_V
                         else f"libqoq_b200_{os.environ['QOQ_LIB_VARIANT']}.so")
 GROUP = 128
 TILE_BYTES = 8448
-ABI_VERSION = 6
+ABI_VERSION = 7
 # kernels launched per call (matches include/qoq_b200.h)
 LAUNCHES = {"quantize_weights": 2, "quantize_activations_per_token": 1, "w4a8_gemm": 1,
             "w4a8_gemm_i32": 1, "pc_quantize_weights": 2, "pc_w4a8_gemm": 1, "pc_w4a8_gemm_i32": 1,
@@ -89,6 +89,8 @@ def load() -> ctypes.CDLL:
             "qoq_linear_chain_workspace_bytes": (Z, [I, I, P]),
             "qoq_w4a8_linear_chain": (I, [I, I, P, P, Z, P]),
             "qoq_debug_reload_knobs": (None, []),
+            "qoq_tp_recv_bytes": (Z, [I, I, I]),
+            "qoq_w4a8_gemm_allreduce": (I, [P, P, P, P, P, I, I, I, I, P, I, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -471,3 +473,63 @@ def w4a8_linear_chain(layers, workspace: Workspace | None = None, stream=None):
     dev = layers[0][0].device
     ws, wsb = _ws_for(dev, nbytes, workspace, kind="chain", stream=stream)
     _check("qoq_w4a8_linear_chain", load().qoq_w4a8_linear_chain(M, len(arr), arr, _ptr(ws), wsb, _stream(stream)))
+
+
+# ------------------------------------------------------------------ fused TP reduction (NEXT-3, ABI v7)
+
+TP_MAX_WORLD = 8
+
+
+class _TpCommC(ctypes.Structure):
+    """include/qoq_b200.h qoq_tp_comm."""
+    _fields_ = [("recv", ctypes.c_void_p * 8), ("gen", ctypes.c_void_p), ("done", ctypes.c_void_p),
+                ("status", ctypes.c_void_p), ("rank", ctypes.c_int), ("world", ctypes.c_int), ("m_cap", ctypes.c_int),
+                ("n_cap", ctypes.c_int)]
+
+
+def tp_recv_bytes(world: int, m_cap: int, n_cap: int) -> int:
+    return int(load().qoq_tp_recv_bytes(world, m_cap, n_cap))
+
+
+class TpComm:
+    """One rank's fused TP reduction (qoq_tp_comm): every rank's receive-buffer pointer (as mapped on this GPU)
+    and this rank's counters. The receive buffers are allocated and shared by the caller (parallel.fused_tp_comm:
+    symmetric memory over the TP group; `local`: one rank)."""
+
+    def __init__(self, rank: int, world: int, recv_ptrs, m_cap: int, n_cap: int, device, keep=()):
+        if not 1 <= world <= TP_MAX_WORLD or not 0 <= rank < world:
+            raise ValueError("need 0 <= rank < world <= 8")
+        self.rank, self.world, self.m_cap, self.n_cap = rank, world, m_cap, n_cap
+        ptrs = [int(v) for v in recv_ptrs]
+        if len(ptrs) != world:
+            raise ValueError("one receive buffer per rank")
+        self.ctr = torch.zeros(64, dtype=torch.int32, device=device)   # gen | done | status (64 B apart)
+        self._keep = keep
+        base = self.ctr.data_ptr()
+        self._c = _TpCommC((ctypes.c_void_p * 8)(*ptrs), base, base + 64, base + 128, rank, world, m_cap, n_cap)
+
+    @classmethod
+    def local(cls, m_cap: int, n_cap: int, device):
+        """world = 1: the reduction of one partial (Y equals w4a8_gemm bit for bit)."""
+        recv = torch.zeros(tp_recv_bytes(1, m_cap, n_cap), dtype=torch.uint8, device=device)
+        return cls(0, 1, [recv.data_ptr()], m_cap, n_cap, device, keep=(recv,))
+
+    def status(self) -> int:
+        """1 if a wait for a peer timed out (after synchronizing)."""
+        return int(self.ctr[32].item())
+
+    def calls(self) -> int:
+        return int(self.ctr[0].item())
+
+
+def w4a8_gemm_allreduce(qx: torch.Tensor, sx: torch.Tensor, tx: torch.Tensor | None, packed: torch.Tensor,
+                        s0: torch.Tensor, N: int, comm: TpComm, out: torch.Tensor | None = None,
+                        stream=None) -> torch.Tensor:
+    """Row-parallel W4A8 GEMM with the TP reduction fused into its epilogue: Y = fp16(Σ_q fp32(Y_q)) over the
+    ranks of `comm`, summed in rank order, identical on every rank (include/qoq_b200.h)."""
+    M, K = qx.shape
+    Y = torch.empty(M, N, dtype=torch.float16, device=qx.device) if out is None else out
+    _check("qoq_w4a8_gemm_allreduce",
+           load().qoq_w4a8_gemm_allreduce(_ptr(qx), _ptr(sx), _ptr(tx), _ptr(packed), _ptr(s0), M, N, K, GROUP,
+                                          _ptr(Y), Y.stride(0), ctypes.byref(comm._c), _stream(stream)))
+    return Y

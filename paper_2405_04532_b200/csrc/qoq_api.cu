@@ -281,6 +281,64 @@ int qoq_w4a8_gemm_i32(const int8_t* qx, const int32_t* tx, const void* packed, i
                     static_cast<cudaStream_t>(stream));
 }
 
+// ---- fused TP reduction of row-parallel partials (NEXT-3)
+
+size_t qoq_tp_recv_bytes(int world, int m_cap, int n_cap) {
+    if (world < 1 || world > QOQ_TP_MAX_WORLD || m_cap < 1 || n_cap < 128 || n_cap % 128) return 0;
+    return 2 * (size_t)world * m_cap * n_cap * 4;   // 8-byte words of two fp16 + a 32-bit flag
+}
+
+// The fused-reduction plan: whole tiles (mode 0, single CTAs), token tile by M alone (16 / 32 / 64 / 128),
+// so every rank of a TP group runs the same tiles with the same CTAs.
+GemmPlan tp_plan(int M, int N, int K, int sms) {
+    GemmPlan p = plan_gemm(M < 128 ? M : 128, N, K, sms);
+    p.MT = (M + p.BN - 1) / p.BN;
+    p.MB = p.MT;
+    p.T = p.MT * p.NT;
+    p.I = (long long)p.T * p.KS;
+    p.mode = 0;
+    p.S = 1;
+    p.CG = 1;
+    p.G = p.T < sms ? p.T : sms;
+    p.ws_bytes = 0;
+    return p;
+}
+
+static_assert(QOQ_TP_MAX_WORLD == kTpMaxWorld, "TP world");
+
+int qoq_w4a8_gemm_allreduce(const int8_t* qx, const void* sx, const int32_t* tx, const void* packed, const void* s0,
+                            int M, int N, int K, int group, void* Y, int ldy, const qoq_tp_comm* comm, void* stream) {
+    int rc = gemm_shape_status(M, N, K, group);
+    if (rc) return rc;
+    if (!comm || comm->world < 1 || comm->world > QOQ_TP_MAX_WORLD || comm->rank < 0 || comm->rank >= comm->world)
+        return QOQ_ERR_INVALID_ARG;
+    if (!comm->gen || !comm->done || !comm->status) return QOQ_ERR_INVALID_ARG;
+    for (int q = 0; q < comm->world; ++q)
+        if (!comm->recv[q] || !aligned16(comm->recv[q])) return QOQ_ERR_INVALID_ARG;
+    if (M > comm->m_cap || N > comm->n_cap || comm->n_cap % 128) return QOQ_ERR_INVALID_ARG;
+    if (M == 0) return QOQ_OK;
+    if (!qx || !sx || !packed || !s0 || !Y || ldy < N || ldy % 4 || !aligned16(Y) || !aligned16(qx) ||
+        !aligned16(packed) || !aligned16(s0))
+        return QOQ_ERR_INVALID_ARG;
+    int sms = 0;
+    if ((rc = check_arch(&sms))) return rc;
+    // whole tiles only (mode 0, single CTAs): the reduction is per output tile, in the tile's epilogue
+    const GemmPlan p = tp_plan(M, N, K, sms);
+    TpComm c{};
+    for (int q = 0; q < comm->world; ++q) c.recv[q] = comm->recv[q];
+    c.gen = comm->gen;
+    c.done = comm->done;
+    c.status = comm->status;
+    c.rank = comm->rank;
+    c.world = comm->world;
+    c.m_cap = comm->m_cap;
+    c.n_cap = comm->n_cap;
+    GemmArgs a{qx, sx, tx, packed, s0, Y, ldy, false, M, N, K, nullptr, nullptr};
+    a.tp = &c;
+    return launch_w4a8_gemm(a, p, static_cast<cudaStream_t>(stream), /*pdl=*/true) == cudaSuccess ? QOQ_OK
+                                                                                                 : QOQ_ERR_CUDA;
+}
+
 size_t qoq_linear_workspace_bytes(int M, int N, int K) {
     if (gemm_shape_status(M, N, K, 128) != QOQ_OK) return 0;
     return linear_ws_layout(nullptr, M, N, K).total;

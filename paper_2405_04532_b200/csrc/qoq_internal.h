@@ -46,6 +46,18 @@ struct Knobs {
 const Knobs& knobs();
 void reload_knobs();
 
+// Device-side view of qoq_tp_comm (include/qoq_b200.h): every rank pushes its fp16 partial of each whole
+// output tile into slot `rank` of every rank's receive buffer (flag-in-data words), then reduces its own
+// slots 0 .. world-1 in rank order (fp32) as their words arrive.
+constexpr int kTpMaxWorld = 8;
+struct TpComm {
+    void* recv[kTpMaxWorld]; // rank q's receive buffer [2][world][m_cap][n_cap/2] 8-B words (kernel parameter)
+    uint32_t* gen;           // this rank's count of completed fused calls (parity; flag = gen + 1)
+    uint32_t* done;          // CTA exit counter of the running call
+    int32_t* status;         // 1 after a peer wait timed out
+    int rank, world, m_cap, n_cap;
+};
+
 struct GemmArgs {
     const int8_t* qx;
     const void* sx;
@@ -66,7 +78,10 @@ struct GemmArgs {
     // per-channel W4A8 (NEXT-1): packed holds 8192-byte code tiles, s0 is s_w, zw the u8 zero points;
     // Y = s_x s_w (acc - z_w t_x) (tx required)
     const uint8_t* zw = nullptr;
+    // fused TP reduction of row-parallel partials (NEXT-3; qoq_w4a8_gemm_allreduce): nullptr = off
+    const TpComm* tp = nullptr;
 };
+
 
 constexpr int kFuseMaxM = 64;   // above: quantizer kernel + GEMM (the prologue would serialize M rows)
 

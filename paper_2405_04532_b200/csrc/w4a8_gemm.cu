@@ -52,12 +52,13 @@ namespace qoq {
 // PC = true: per-channel W4A8 (NEXT-1, §5.2.2): 8192-byte code tiles, no level-2 parameters; the
 // dequant only unpacks (lanes = q_u4, fed as UNSIGNED 8-bit A) and the epilogue applies the zero
 // point after the multiplication: Y = s_x s_w (acc - z_w t_x).
-template <int BN, int CG = 1, bool PC = false>
+template <int BN, int CG = 1, bool PC = false, bool TP = false>
 struct Cfg {
     static constexpr int kTB = PC ? kPcTileBytes : kTileBytes;        // bytes of one packed 128x128 tile
     // dequant groups: QOQ_DEQ_GROUPS (default 3; measured +1..9% over 2 at decode) where the TMEM budget allows a rotation-compatible
-    // A ring, else 2
-    static constexpr int kDeqGroups = (BN <= 64) ? QOQ_DEQ_GROUPS : 2;
+    // A ring, else 2. TP (fused reduction, short K shards): 2, so the 448-thread CTA has 144 registers for the
+    // reduction's loads in flight (3 groups = 640 threads at the 96-register cap)
+    static constexpr int kDeqGroups = (BN <= 64 && !TP) ? QOQ_DEQ_GROUPS : 2;
     using R = Roles<kDeqGroups>;
     static constexpr int kBlockThreads = R::kBlockThreads;
 #ifndef QOQ_ISSUERS_BIG
@@ -156,6 +157,7 @@ struct KParams {
     int ldx, K;
     int* qsync;                  // [2] arrivals / departures; the last departure re-zeroes both
     const uint8_t* zw;           // per-channel W4A8: z_w [N] (else nullptr)
+    TpComm tp;                   // fused TP reduction (NEXT-3, the TP instantiation): whole tiles, CG = 1, fp16 out
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -414,15 +416,71 @@ __device__ __forceinline__ void fused_depart(const KParams& p) {
     }
 }
 
+// ---------------------------------------------------------------- fused TP reduction (NEXT-3)
+// Row-parallel layers (o, down) end in Y = Σ_r Y_r over the TP ranks (north_star). Instead of a separate
+// all-reduce, each rank's epilogue PUSHES its fp16 partial of every whole tile into slot `rank` of every
+// rank's receive buffer (peer stores over NVLink; the buffers are symmetric allocations) and then reduces
+// its own slots 0 .. world-1 in rank order in fp32, rounding once to fp16 (reading Q32: deterministic,
+// identical bits on every rank). The slots are in a flag-in-data format: every 8-byte word carries two
+// fp16 values and the call's flag (gen + 1), written by ONE 16-byte relaxed system-scope store per four
+// outputs, so a reader knows a word has landed by its flag alone — no fence, no counter, no barrier (a
+// release fence costs microseconds on an SM with memory in flight). The buffers alternate by call parity:
+// a rank can be at most one call ahead of a peer (it needs the peer's partials to finish a call), so the
+// buffer it writes is never the one the peer still reads.
+__device__ __forceinline__ size_t tp_word(const TpComm& c, int par, int slot, int m, int n) {
+    // 8-byte words [2 parities][world slots][m_cap][n_cap / 2]; (m, n) with n % 4 == 0 -> words n/2, n/2 + 1
+    return (((size_t)par * c.world + slot) * c.m_cap + m) * (c.n_cap / 2) + n / 2;
+}
+__device__ __forceinline__ void st_relaxed_sys_v4(void* p, uint4 v) {
+    asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint4 ld_relaxed_sys_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p) : "memory");
+    return v;
+}
+// Re-poll one 16-byte pair of words until both carry `flag`. Peers are other GPUs: a wait beyond 2 s (a peer
+// not running the same call sequence) sets the status word and gives up instead of hanging the device.
+__device__ __forceinline__ uint4 tp_poll(const TpComm& c, const void* w, uint32_t flag) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (uint32_t n = 1;; ++n) {
+        const uint4 v = ld_relaxed_sys_v4(w);
+        if (v.y == flag && v.w == flag) return v;
+        if ((n & 255u) == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 2000000000ull) {
+                atomicExch(c.status, 1);
+                return make_uint4(0u, flag, 0u, flag);
+            }
+        }
+        __nanosleep(20);
+    }
+}
+__device__ __forceinline__ uint2 y4_bits(int4 a, int bias, float sxf, const float (&s0v)[4], const int (&zv)[4]) {
+    a.x -= bias * zv[0]; a.y -= bias * zv[1]; a.z -= bias * zv[2]; a.w -= bias * zv[3];
+    __half2 lo = __halves2half2(__float2half_rn((float)a.x * (sxf * s0v[0])), __float2half_rn((float)a.y * (sxf * s0v[1])));
+    __half2 hi = __halves2half2(__float2half_rn((float)a.z * (sxf * s0v[2])), __float2half_rn((float)a.w * (sxf * s0v[3])));
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    return u;
+}
+
 template <int BN>
 __device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<BN, 1>::kChunk]) {
     tmem_ld_cols<Cfg<BN, 1>::kChunk>(taddr, v);
 }
 
-template <int BN, bool OUT_I32, int CG, bool PC = false>
-__global__ void __launch_bounds__(Cfg<BN, CG, PC>::kBlockThreads, 1)
+// TP = true: the fused TP reduction (NEXT-3) — its own instantiation, so the other kernels carry none of its
+// registers (the BN <= 64 kernels run 640 threads at the 96-register cap)
+template <int BN, bool OUT_I32, int CG, bool PC = false, bool TP = false>
+__global__ void __launch_bounds__(Cfg<BN, CG, PC, TP>::kBlockThreads, 1)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
-    using C = Cfg<BN, CG, PC>;
+    using C = Cfg<BN, CG, PC, TP>;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B aligned base derived by pointer arithmetic on the __shared__ array, so the compiler keeps
     // the shared address space (LDS/STS, not generic LD/ST) for everything carved from it
@@ -729,6 +787,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC>::kBlockThreads, 1)
         }
         pdl_wait();
         if (et == 0) QOQ_TRACE(p, 12);
+        // fused TP reduction: this call's parity and expected flag count (gen was advanced by the previous
+        // fused call's last CTA, complete before griddepcontrol.wait returns)
+        uint32_t tp_par = 0, tp_flag = 0;
+        if constexpr (TP) {
+            const uint32_t gen = __ldcg(p.tp.gen);
+            tp_par = gen & 1u;
+            tp_flag = gen + 1u;
+        }
         if (p.X) {   // fused per-token quantization of X, then the grid handshake (s_x / t_x below)
             fused_quantize_rows(p, et, sxs, txs);
             if (et == 0) {
@@ -888,6 +954,24 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC>::kBlockThreads, 1)
                         bulk_reduce_add_s32(wst + (size_t)j0 * 128, sb, C::kStgBytes);
                         bulk_commit();
                     }
+                } else if constexpr (TP) {
+                    // NEXT-3: this rank's partial -> slot `rank` of every rank, one 16-byte flag-in-data store per
+                    // 4 outputs and rank; all shared-memory reads first, as in the plain write-out
+                    named_bar_sync(1, 128);
+                    constexpr int kU = C::kChunk / 4;
+                    int4 av[kU];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) av[u] = *reinterpret_cast<const int4*>(sb + (g + 4 * u) * 128 + 4 * l);
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const int jj = g + 4 * u, m = m0 + j0 + jj;
+                        if (m >= p.M) break;
+                        const uint2 y = y4_bits(av[u], txs[j0 + jj], sxs[j0 + jj], s0v, z0v);
+                        const uint4 w = make_uint4(y.x, tp_flag, y.y, tp_flag);
+                        const size_t off = tp_word(p.tp, tp_par, p.tp.rank, m, n0 + 4 * l);
+#pragma unroll 1
+                        for (int q = 0; q < p.tp.world; ++q) st_relaxed_sys_v4(static_cast<uint2*>(p.tp.recv[q]) + off, w);
+                    }
                 } else {
                     named_bar_sync(1, 128);
                     // all shared-memory reads first, then the stores: the (m < M) guards would
@@ -913,6 +997,49 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC>::kBlockThreads, 1)
                 }
             }
             if (et == 0) QOQ_TRACE(p, 26);
+            if constexpr (TP) {
+                // reduce in rank order (fp32, one rounding to fp16): thread (g, l) owns Y[m][n0 + 4l .. +3] for
+                // the tile's tokens m = m0 + g + 4j (the write-out mapping, so its own slot's words are its own
+                // earlier stores); each word is valid once it carries this call's flag. kB tokens per batch:
+                // all of a batch's loads of one slot in flight, then only the missing words re-polled
+                const uint2* rb = static_cast<const uint2*>(p.tp.recv[p.tp.rank]);
+                constexpr int kB = BN / 4 < 4 ? BN / 4 : 4;
+#pragma unroll 1
+                for (int j0 = g; j0 < BN && m0 + j0 < p.M; j0 += 4 * kB) {
+                    const int n = n0 + 4 * l;
+                    float a[kB][4];
+#pragma unroll 1
+                    for (int q = 0; q < p.tp.world; ++q) {
+                        uint4 v[kB];
+#pragma unroll
+                        for (int b = 0; b < kB; ++b) {
+                            const int m = m0 + j0 + 4 * b;
+                            v[b] = (j0 + 4 * b < BN && m < p.M) ? ld_relaxed_sys_v4(rb + tp_word(p.tp, tp_par, q, m, n))
+                                                                : make_uint4(0u, tp_flag, 0u, tp_flag);
+                        }
+#pragma unroll
+                        for (int b = 0; b < kB; ++b) {
+                            if (v[b].y != tp_flag || v[b].w != tp_flag)
+                                v[b] = tp_poll(p.tp, rb + tp_word(p.tp, tp_par, q, m0 + j0 + 4 * b, n), tp_flag);
+                            const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&v[b].x));
+                            const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&v[b].z));
+                            if (q == 0) { a[b][0] = f0.x; a[b][1] = f0.y; a[b][2] = f1.x; a[b][3] = f1.y; }
+                            else { a[b][0] += f0.x; a[b][1] += f0.y; a[b][2] += f1.x; a[b][3] += f1.y; }
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < kB; ++b) {
+                        const int m = m0 + j0 + 4 * b;
+                        if (j0 + 4 * b >= BN || m >= p.M) continue;
+                        __half2 lo = __halves2half2(__float2half_rn(a[b][0]), __float2half_rn(a[b][1]));
+                        __half2 hi = __halves2half2(__float2half_rn(a[b][2]), __float2half_rn(a[b][3]));
+                        uint2 u;
+                        u.x = *reinterpret_cast<uint32_t*>(&lo);
+                        u.y = *reinterpret_cast<uint32_t*>(&hi);
+                        *reinterpret_cast<uint2*>(static_cast<__half*>(p.out) + (size_t)m * p.ldo + n) = u;
+                    }
+                }
+            }
             if (++cst == C::kAccStages) { cst = 0; cph ^= 1; }
             if (!whole) {
                 if (et == 0) {
@@ -949,6 +1076,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC>::kBlockThreads, 1)
             if (et == 0) QOQ_TRACE(p, 8);
         }
         if (et == 0) bulk_wait<0>();
+        // fused TP reduction: the last CTA out advances this rank's call counter (read by the next fused call
+        // after its griddepcontrol.wait)
+        if (TP && et == 0) {   // (no fence: the next call reads gen after grid completion)
+            if (atomicAdd(p.tp.done, 1u) == gridDim.x - 1) {
+                *p.tp.done = 0u;
+                atomicAdd(p.tp.gen, 1u);
+            }
+        }
     }
 
     tc_fence_before();
@@ -1130,10 +1265,10 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     return p;
 }
 
-template <int BN, bool OUT_I32, int CG, bool PC = false>
+template <int BN, bool OUT_I32, int CG, bool PC = false, bool TP = false>
 static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t st, bool pdl) {
-    using C = Cfg<BN, CG, PC>;
-    auto kern = w4a8_gemm_kernel<BN, OUT_I32, CG, PC>;
+    using C = Cfg<BN, CG, PC, TP>;
+    auto kern = w4a8_gemm_kernel<BN, OUT_I32, CG, PC, TP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     auto enc = tensor_map_encoder();
@@ -1174,6 +1309,7 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
     kp.K = a.K;
     kp.qsync = a.qsync;
     kp.zw = a.zw;
+    if (TP) kp.tp = *a.tp;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.G * CG);
     cfg.blockDim = dim3(C::kBlockThreads);
@@ -1200,6 +1336,11 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
 
 template <int BN>
 static cudaError_t launch_bn_cg(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl) {
+    if (a.tp) {   // fused TP reduction: whole tiles, single CTAs, fp16 out (tp_plan)
+        if (p.CG != 1 || p.mode != 0 || a.out_i32 || a.zw) return cudaErrorInvalidValue;
+        if constexpr (BN <= 128) return launch_bn<BN, false, 1, false, true>(a, p, st, pdl);
+        return cudaErrorInvalidValue;
+    }
     if (a.zw) {   // per-channel W4A8: single-CTA tiles only
         if (p.CG != 1) return cudaErrorInvalidValue;
         return a.out_i32 ? launch_bn<BN, true, 1, true>(a, p, st, pdl) : launch_bn<BN, false, 1, true>(a, p, st, pdl);

@@ -160,17 +160,40 @@ def shard_layer(packed_layer, plan, rank: int, world: int):
     return out
 
 
-def tp_decode_layer(inputs, shards, plan, linear, all_reduce, rank: int, world: int):
+def tp_decode_layer(inputs, shards, plan, linear, all_reduce, rank: int, world: int, fused_rows: bool = False):
     """One decode layer of the benchmark step on this rank, in order (qkv, o, gate_up, down):
     X = inputs[quant_group] (replicated [M][K]; a row-parallel rank reads its K-shard view), then
     Y = linear(X_r, shard, plan_entry) (quantize X_r per token + W4A8 GEMM), then one all_reduce of Y after
-    each row-parallel linear. Returns {name: Y}."""
+    each row-parallel linear — unless fused_rows: then the row-parallel `linear` already returns the reduced
+    Y (qoq_w4a8_gemm_allreduce, NEXT-3) and no separate collective runs. Returns {name: Y}."""
     out = {}
     for shard, entry in zip(shards, plan):
         name, Nr, Kr, N, K, kind, qg = entry
         X_r = shard_input(inputs[qg], kind, rank, world)
         Y = linear(X_r, shard, entry)
-        if kind == "row" and world > 1:
+        if kind == "row" and world > 1 and not fused_rows:
             all_reduce(Y)
         out[name] = Y
     return out
+
+
+# ------------------------------------------------------------------ fused TP reduction (NEXT-3)
+
+def fused_tp_comm(qoq, group, m_cap: int, n_cap: int, device):
+    """The rank's qoq.TpComm over `group`: one symmetric-memory receive buffer per rank (torch.distributed's
+    _symmetric_memory: peer-mapped over NVLink), zeroed, exchanged with a rendezvous, so every rank's buffer
+    is addressable from every GPU. Collective over `group`."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    nbytes = qoq.tp_recv_bytes(world, m_cap, n_cap)
+    if nbytes <= 0:
+        raise ValueError("unsupported fused-reduction capacity")
+    buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+    buf.zero_()
+    hdl = symm_mem.rendezvous(buf, group)
+    torch.cuda.synchronize(device)
+    dist.barrier(group)          # every rank's buffer is zero before any peer pushes into it
+    return qoq.TpComm(rank, world, [int(p) for p in hdl.buffer_ptrs], m_cap, n_cap, device, keep=(buf, hdl))

@@ -45,7 +45,7 @@ def test_library_is_sm100a_only(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert lib.qoq_abi_version() == 6
+    assert lib.qoq_abi_version() == 7
     for s in range(0, 8):
         assert lib.qoq_status_string(s)
 
@@ -183,3 +183,31 @@ def test_linear_chain_validation(lib):
     assert lib.qoq_w4a8_linear_chain(64, 1, bad_al, P(fake), Z(1 << 30), None) == 1
     null_y = (D * 1)(D(fake, 4096, 128, 4096, fake, fake, None, 128))
     assert lib.qoq_w4a8_linear_chain(64, 1, null_y, P(fake), Z(1 << 30), None) == 1
+
+
+def test_fused_tp_reduction_sizes_and_validation(lib):
+    """NEXT-3 entry: capacity query, and every comm / capacity violation rejected on the host."""
+    import paper_2405_04532_b200 as qoq
+    assert lib.qoq_tp_recv_bytes(8, 64, 4096) == 2 * 8 * 64 * 4096 * 4   # flag-in-data words: 4 B per fp16
+    assert lib.qoq_tp_recv_bytes(9, 64, 4096) == 0 and lib.qoq_tp_recv_bytes(2, 64, 100) == 0
+    assert lib.qoq_tp_recv_bytes(2, 0, 4096) == 0
+    P = ctypes.c_void_p
+    fake = P(1 << 20)
+
+    def comm(rank=0, world=2, m_cap=64, n_cap=4096, null=False):
+        recv = (ctypes.c_void_p * 8)(*([1 << 20] * 8))
+        if null:
+            recv[1] = None
+        return qoq._TpCommC(recv, 1 << 20, 1 << 20, 1 << 20, rank, world, m_cap, n_cap)
+
+    def call(c, M=64, N=4096, K=512, group=128, ldy=4096):
+        return lib.qoq_w4a8_gemm_allreduce(fake, fake, None, fake, fake, M, N, K, group, fake, ldy,
+                                           ctypes.byref(c) if c is not None else None, None)
+
+    assert call(None) == 1
+    assert call(comm(world=9)) == 1 and call(comm(rank=2)) == 1 and call(comm(rank=-1)) == 1
+    assert call(comm(null=True)) == 1
+    assert call(comm(m_cap=32)) == 1 and call(comm(n_cap=2048)) == 1 and call(comm(n_cap=4160)) == 1
+    assert call(comm(), ldy=4000) == 1
+    assert call(comm(), group=64) == 3 and call(comm(), K=500) == 2
+    assert call(comm(), M=0) == 0   # nothing to do

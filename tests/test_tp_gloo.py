@@ -313,3 +313,68 @@ def test_bench_step_tp_path_gloo():
         assert np.all(np.abs(y - ref) <= RTOL * np.abs(ref) + ATOL), name
         assert np.linalg.norm(y - one[name]) / np.linalg.norm(one[name]) < 0.05
     assert a0 > 0
+
+
+def _fused_step_worker(rank, world, port, M, out_q):
+    """bench.py's fused-reduction step (NEXT-3) with the oracle as the rank's device: a row-parallel linear
+    returns the REDUCED output itself (its partial, gathered from every rank, summed in rank order as
+    qoq_w4a8_gemm_allreduce does), so tp_decode_layer(fused_rows=True) issues no separate all-reduce."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shapes, inputs = _step_inputs(M)
+        plan = parallel.rank_layer_plan(shapes, world)
+        shards = parallel.shard_layer(_step_weights(shapes), plan, rank, world)
+
+        def linear(X_r, shard, entry):
+            Y = _step_linear(X_r, shard, entry)
+            if entry[5] != "row":
+                return Y
+            parts = [torch.empty_like(Y) for _ in range(world)]
+            dist.all_gather(parts, Y)
+            return torch.from_numpy(oracle.tp_reduce_rank_order([p.numpy() for p in parts]))
+
+        def no_collective(Y):
+            raise AssertionError("fused_rows must not issue a separate all-reduce")
+
+        out = parallel.tp_decode_layer(inputs, shards, plan, linear, no_collective, rank, world, fused_rows=True)
+        out_q.put((rank, {k: v.numpy() for k, v in out.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_reduction_step_gloo():
+    """The NEXT-3 step at TP = 2: every rank ends with bit-identical o / down outputs (rank-order fp32 sum of
+    the fp16 partials, reading Q32), within tolerance of the fp64 sum of the per-rank exact results."""
+    M, world = 8, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_step_worker, args=(r, world, port, M, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shapes, inputs = _step_inputs(M)
+    full = _step_weights(shapes)
+    plan = parallel.rank_layer_plan(shapes, world)
+    for name in ("o", "down"):
+        assert np.array_equal(res[0][name].view(np.uint16), res[1][name].view(np.uint16))
+        i = [e[0] for e in plan].index(name)
+        _, Nr, Kr, N, K, kind, qg = plan[i]
+        refs = []
+        for r in range(world):
+            p_r, s0_r = parallel.shard_layer(full, plan, r, world)[i]
+            X_r = np.ascontiguousarray(parallel.shard_input(inputs[qg], kind, r, world))
+            qx, sx, tx = oracle.quantize_activations(X_r)
+            refs.append(oracle.epilogue_f64(oracle.acc_from_packed(qx, np.ascontiguousarray(p_r), N, Kr), sx,
+                                            np.ascontiguousarray(s0_r)))
+        ref = sum(refs)
+        y = res[0][name].astype(np.float64)
+        # each fp16 partial within the north_star tolerance of its exact value, plus the final fp16 rounding
+        bound = sum(RTOL * np.abs(r) + ATOL for r in refs) + 2.0 ** -11 * np.abs(ref)
+        assert np.all(np.abs(y - ref) <= bound)
+
