@@ -6,11 +6,16 @@
 //   2  TMA bulk multicast, cluster of 4
 //   3  LSU: 4 warps ld.global.v4 + st.shared (no TMA for activations)
 //   4  no activations (weights only)
+//   5  TMA 2-D tensor loads (box 128 B x 64 rows, SWIZZLE_128B, two per step) from a row-major [64][4096] q_x,
+//      as the GEMM's activation producer does
+//   6  as 5, issued by the weight producer thread itself (one TMA issuer)
 // Prints weight bytes per cycle per SM and the aggregate weight TB/s.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/ingress_bench2.cu -o tools/ingress_bench2
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -46,8 +51,8 @@ __device__ __forceinline__ void bulk_mc(void* dst, const void* src, uint32_t byt
 
 constexpr int kW = 16896, kWS = 17408, kWR = 6, kX = 16384, kXR = 5, kIters = 300;
 
-__global__ void __launch_bounds__(224, 1) pipe(const uint8_t* w, size_t per, const uint8_t* act, int variant, int C,
-                                               long long* cyc) {
+__global__ void __launch_bounds__(224, 1) pipe(const __grid_constant__ CUtensorMap tmx, const uint8_t* w, size_t per,
+                                               const uint8_t* act, int variant, int C, long long* cyc) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ __align__(8) uint64_t wfull[kWR], wfree[kWR], xfull[kXR], xfree[kXR];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -77,8 +82,27 @@ __global__ void __launch_bounds__(224, 1) pipe(const uint8_t* w, size_t per, con
             if (it >= kWR) wait(&wfree[i], ((it / kWR) - 1) & 1);
             expect(&wfull[i], kW);
             bulk(sm + i * kWS, base + (size_t)it * kW, kW, &wfull[i]);
+            if (variant == 6) {
+                const int j = it % kXR;
+                if (it >= kXR) wait(&xfree[j], ((it / kXR) - 1) & 1);
+                expect(&xfull[j], kX);
+                for (int t = 0; t < 2; ++t)
+                    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                                 ::"r"(smem_u32(xs + j * kX + t * 8192)), "l"(&tmx), "r"(((2 * it + t) % 32) * 128), "r"(0),
+                                 "r"(smem_u32(&xfull[j])) : "memory");
+            }
         }
-    } else if (warp == 1 && lane == 0 && acts && variant != 3) {   // activation producer (TMA)
+    } else if (warp == 1 && lane == 0 && variant == 5) {   // activation producer: 2-D tensor loads
+        for (int it = 0; it < kIters; ++it) {
+            const int i = it % kXR;
+            if (it >= kXR) wait(&xfree[i], ((it / kXR) - 1) & 1);
+            expect(&xfull[i], kX);
+            for (int t = 0; t < 2; ++t)
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                             ::"r"(smem_u32(xs + i * kX + t * 8192)), "l"(&tmx), "r"(((2 * it + t) % 32) * 128), "r"(0),
+                             "r"(smem_u32(&xfull[i])) : "memory");
+        }
+    } else if (warp == 1 && lane == 0 && acts && variant != 3 && variant != 6) {   // activation producer (TMA)
         for (int it = 0; it < kIters; ++it) {
             const int i = it % kXR;
             if (it >= kXR) wait(&xfree[i], ((it / kXR) - 1) & 1);
@@ -135,12 +159,29 @@ int main() {
     cudaMalloc(&act, 16 * kX);
     cudaMemset(act, 2, 16 * kX);
     cudaMalloc(&cyc, 8 * 148);
-    const int smem = kWR * kWS + kXR * kX + 1024;
+    const int smem = kWR * kWS + kXR * kX + 2048;
     cudaFuncSetAttribute(pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(pipe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    const char* names[5] = {"TMA own", "TMA mcast2", "TMA mcast4", "LSU acts", "no acts"};
+    const char* names[7] = {"TMA own", "TMA mcast2", "TMA mcast4", "LSU acts", "no acts", "TMA 2-D", "2-D 1 issuer"};
+    // q_x [64][4096] int8 row-major, box {128, 64}, SWIZZLE_128B (the GEMM's activation map at M = 64)
+    uint8_t* qx;
+    cudaMalloc(&qx, 64 * 4096);
+    cudaMemset(qx, 3, 64 * 4096);
+    CUtensorMap tm;
+    {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+        auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        cuuint64_t dims[2] = {4096, 64};
+        cuuint64_t strides[1] = {4096};
+        cuuint32_t box[2] = {128, 64};
+        cuuint32_t es[2] = {1, 1};
+        enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, qx, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     for (int G : {32, 64, 128, 148}) {
-        for (int variant = 0; variant < 5; ++variant) {
+        for (int variant : {0, 3, 4, 5, 6}) {
             const int C = variant == 1 ? 2 : variant == 2 ? 4 : 1;
             if (G % C) continue;
             long long hc[148];
@@ -157,7 +198,7 @@ int main() {
                 at[0].val.clusterDim.z = 1;
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
-                e = cudaLaunchKernelEx(&cfg, pipe, (const uint8_t*)w, per, (const uint8_t*)act, variant, C, cyc);
+                e = cudaLaunchKernelEx(&cfg, pipe, tm, (const uint8_t*)w, per, (const uint8_t*)act, variant, C, cyc);
                 if (e == cudaSuccess) e = cudaDeviceSynchronize();
             }
             if (e != cudaSuccess) {
