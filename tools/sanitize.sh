@@ -5,8 +5,9 @@
 cd "$(dirname "$0")/.."
 OUT=${1:-gpurun_out}
 CS=/usr/local/cuda/bin/compute-sanitizer
+CASES=${CASES:-gemm_mode0 gemm_mode1 gemm_mode2 gemm_cg2 gemm_prefill fused_linear per_channel quantizers kv4 chain tp_fused}
 for tool in memcheck racecheck synccheck initcheck; do
-  for c in gemm_mode0 gemm_mode1 gemm_mode2 gemm_cg2 gemm_prefill fused_linear per_channel quantizers kv4 chain; do
+  for c in $CASES; do
     echo "=== $tool $c"
     timeout 600 $CS --tool $tool --print-limit 20 python tools/sanitize_cases.py --case $c 2>&1 | \
       grep -E "ERROR SUMMARY|RACECHECK SUMMARY|case .*: ok|Error|error|Hazard|hazard|Timeout|Killed" | head -20

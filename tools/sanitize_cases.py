@@ -104,10 +104,24 @@ def chain(M=16):
         assert torch.equal(r, Y)
 
 
+def tp_fused(M=16, N=256, K=512):
+    """NEXT-3: the fused TP reduction at world 1 (push + flag-in-data words + rank-order reduce, all local)
+    equals the plain GEMM, over both buffer parities."""
+    gen = torch.Generator(device=dev).manual_seed(3)
+    p, s0 = qoq.quantize_weights(synth.device_weights_fp16(N, K, gen, dev))
+    qx, sx, tx = qoq.quantize_activations_per_token(synth.device_activations_fp16(M, K, gen, dev))
+    ref = qoq.w4a8_gemm(qx, sx, tx, p, s0, N)
+    comm = qoq.TpComm.local(M, N, dev)
+    for _ in range(2):
+        y = qoq.w4a8_gemm_allreduce(qx, sx, tx, p, s0, N, comm)
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref) and comm.status() == 0
+
+
 CASES = {"gemm_mode0": lambda: gemm(mode=0), "gemm_mode1": lambda: gemm(mode=1, M=64, N=256, K=1024),
          "gemm_mode2": lambda: gemm(mode=2, M=16, N=256, K=1024), "gemm_cg2": lambda: gemm(cg=2, M=64, N=256, K=512),
          "gemm_prefill": lambda: gemm(M=300, N=256, K=256), "fused_linear": fused_linear, "per_channel": per_channel,
-         "quantizers": quantizers, "kv4": kv4, "chain": chain}
+         "quantizers": quantizers, "kv4": kv4, "chain": chain, "tp_fused": tp_fused}
 
 
 if __name__ == "__main__":
