@@ -3,10 +3,10 @@
 One GPU is available here, so the cross-rank protocol is exercised without ranks that wait on one another:
   * world = 1: the push, the flag and the wait are local; Y must equal qoq_w4a8_gemm bit for bit, call after
     call (parities alternate, the call counter advances), also under CUDA-graph replay;
-  * world = 2 with a pre-seeded peer: the peer's partial, in the flag-in-data word format with this call's
-    flag, is written into this rank's buffer BEFORE the single kernel runs (what the peer's kernel would have
-    stored); this rank's kernel must store its own partial (with the flag) into the peer's slot and reduce
-    in rank order exactly as oracle.tp_reduce_rank_order; run as rank 0 and as rank 1, over 3 calls;
+  * world = 2, 4, 8 with pre-seeded peers: every peer's partial, in the flag-in-data word format with this
+    call's flag, is written into this rank's buffer BEFORE the single kernel runs (what the peers' kernels
+    would have stored); this rank's kernel must store its own partial (with the flag) into every rank's slot
+    and reduce in rank order exactly as oracle.tp_reduce_rank_order; as first, middle and last rank, 3 calls;
   * a peer whose words never arrive: the wait gives up after 2 s and sets the status word (no hang).
 A real multi-GPU run (torchrun, NCCL + symmetric memory) is test_fused_reduction_multi_gpu, skipped with < 2 GPUs.
 """
@@ -90,13 +90,13 @@ def test_world1_cuda_graph_replay(gpu_lib):
     assert comm.status() == 0 and comm.calls() == 1 + 3 * 4
 
 
-def _two_rank_buffers(gpu_lib, M, N):
-    return [torch.zeros(gpu_lib.tp_recv_bytes(2, M, N) // 4, dtype=torch.int32, device=dev()) for _ in range(2)]
+def _rank_buffers(gpu_lib, M, N, world):
+    return [torch.zeros(gpu_lib.tp_recv_bytes(world, M, N) // 4, dtype=torch.int32, device=dev()) for _ in range(world)]
 
 
-def _words(buf, par, slot, M, N):
-    """Slot `slot` of parity `par` of a 2-rank receive buffer as [M][N/2] 8-byte words {2 fp16, flag}."""
-    return buf.view(2, 2, M, N // 2, 2)[par, slot]
+def _words(buf, par, slot, M, N, world=2):
+    """Slot `slot` of parity `par` of a receive buffer as [M][N/2] 8-byte words {2 fp16, flag}."""
+    return buf.view(2, world, M, N // 2, 2)[par, slot]
 
 
 def _ll(Y, flag):
@@ -108,36 +108,34 @@ def _ll(Y, flag):
     return w
 
 
-@pytest.mark.parametrize("me", [0, 1])
+@pytest.mark.parametrize("world,me", [(2, 0), (2, 1), (4, 2), (8, 0), (8, 7)])
 @pytest.mark.parametrize("M,N,K", [(64, 4096, 512), (5, 512, 1792), (33, 1280, 256)])
-def test_world2_preseeded_peer_rank_order(gpu_lib, me, M, N, K):
-    peer = 1 - me
-    mine = _rank_inputs(M, N, K, seed=100 + M)
-    theirs = _rank_inputs(M, N, K, seed=200 + M)
-    Y_me = _partial(M, N, K, mine)
-    Y_peer = _partial(M, N, K, theirs)
-    recv = _two_rank_buffers(gpu_lib, M, N)
-    comm = gpu_lib.TpComm(me, 2, [r.data_ptr() for r in recv], M, N, dev(), keep=(recv,))
-    p, s0, qx, sx, tx = (to_dev(a) for a in mine)
-    order = [None, None]
-    order[me], order[peer] = Y_me.cpu().numpy(), Y_peer.cpu().numpy()
-    want = torch.from_numpy(oracle.tp_reduce_rank_order(order)).to(dev())
+def test_preseeded_peers_rank_order(gpu_lib, world, me, M, N, K):
+    """One rank's kernel with world - 1 pre-seeded peers: every peer's partial (this call's flag) is in our buffer
+    before the kernel runs; our partial must land in every peer's slot `me`, and Y must equal the rank-order
+    reduction bit for bit."""
+    cases = [_rank_inputs(M, N, K, seed=100 * (r + 1) + M) for r in range(world)]
+    parts = [_partial(M, N, K, c) for c in cases]
+    recv = _rank_buffers(gpu_lib, M, N, world)
+    comm = gpu_lib.TpComm(me, world, [r.data_ptr() for r in recv], M, N, dev(), keep=(recv,))
+    p, s0, qx, sx, tx = (to_dev(a) for a in cases[me])
+    want = torch.from_numpy(oracle.tp_reduce_rank_order([y.cpu().numpy() for y in parts])).to(dev())
     for call in range(3):
         par, flag = call & 1, call + 1
-        # what the peer's kernel stores before our reduction can finish: its partial, with this call's flag,
-        # in OUR slot `peer` (a stale flag would make us wait)
-        _words(recv[me], par, peer, M, N).copy_(_ll(Y_peer, flag))
+        for q in range(world):   # what the peers' kernels store into OUR buffer (a stale flag would make us wait)
+            if q != me:
+                _words(recv[me], par, q, M, N, world).copy_(_ll(parts[q], flag))
         torch.cuda.synchronize()
         Y = gpu_lib.w4a8_gemm_allreduce(qx, sx, tx, p, s0, N, comm)
         torch.cuda.synchronize()
         assert comm.status() == 0
         assert torch.equal(Y, want), f"call {call}: rank-order reduction differs"
-        # our push landed in the peer's slot `me`: exactly the plain GEMM's partial, with this call's flag
-        assert torch.equal(_words(recv[peer], par, me, M, N), _ll(Y_me, flag))
-    # and the result is within the propagated north_star tolerance of the exact sum of the two exact partials:
-    # each fp16 partial is within RTOL |ref_q| + ATOL of its exact value, plus the final fp16 rounding
-    refs = [oracle.epilogue_f64(oracle.acc_from_packed(c[2], c[0], N, K), c[3], c[1]) for c in (mine, theirs)]
-    ref = refs[0] + refs[1]
+        for q in range(world):   # our partial, with this call's flag, in every rank's slot `me`
+            assert torch.equal(_words(recv[q], par, me, M, N, world), _ll(parts[me], flag))
+    # within the propagated north_star tolerance of the exact sum of the exact partials: each fp16 partial is
+    # within RTOL |ref_q| + ATOL of its exact value, plus the final fp16 rounding
+    refs = [oracle.epilogue_f64(oracle.acc_from_packed(c[2], c[0], N, K), c[3], c[1]) for c in cases]
+    ref = sum(refs)
     y = Y.cpu().numpy().astype(np.float64)
     bound = sum(RTOL * np.abs(r) + ATOL for r in refs) + 2.0 ** -11 * np.abs(ref)
     assert np.all(np.abs(y - ref) <= bound)
@@ -148,7 +146,7 @@ def test_world2_stale_peer_times_out_without_hanging(gpu_lib):
     call's flag, gives up after 2 s and sets the status word instead of hanging."""
     M, N, K = 16, 256, 256
     mine = _rank_inputs(M, N, K, seed=9)
-    recv = _two_rank_buffers(gpu_lib, M, N)
+    recv = _rank_buffers(gpu_lib, M, N, 2)
     comm = gpu_lib.TpComm(0, 2, [r.data_ptr() for r in recv], M, N, dev(), keep=(recv,))
     p, s0, qx, sx, tx = (to_dev(a) for a in mine)
     gpu_lib.w4a8_gemm_allreduce(qx, sx, tx, p, s0, N, comm)
