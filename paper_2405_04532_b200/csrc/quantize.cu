@@ -193,8 +193,17 @@ __global__ void __launch_bounds__(128) pc_pack_kernel(const __half* __restrict__
 // the dependent GEMM, which PDL releases at entry: its CTAs stream their static weights while this
 // kernel runs and read q_x only after griddepcontrol.wait. (Measured on the decode step: splitting
 // rows over clusters to use more SMs, or capping registers to co-reside with GEMM CTAs, was slower.)
-constexpr int kQThreads = 256;
-constexpr int kQVec = 8;
+// 512 threads x 4 vectors (K <= 16384 from registers). Measured on the decode step (M = 64, Llama-3-8B,
+// profiles/r2b_quantizer_threads.txt): 1.737 ms against 1.814 ms with 256 x 8 — 2.70 / 4.94 us per launch at
+// K = 4096 / 14336 instead of 3.02 / 5.57 (384, 640, 768 and 1024 threads were within 1-3% or slower).
+#ifndef QOQ_QTHREADS
+#define QOQ_QTHREADS 512
+#endif
+#ifndef QOQ_QVEC
+#define QOQ_QVEC 4
+#endif
+constexpr int kQThreads = QOQ_QTHREADS;   // (build knobs for A/B: threads per row, 16-byte vectors per thread)
+constexpr int kQVec = QOQ_QVEC;
 
 __global__ void __launch_bounds__(kQThreads) quantize_act_kernel(const __half* __restrict__ X, int K, int ldx,
                                                                  int8_t* __restrict__ qx, __half* __restrict__ sx,
