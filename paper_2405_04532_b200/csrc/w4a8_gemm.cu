@@ -852,10 +852,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC, TP>::kBlockThreads, 1)
                         *reinterpret_cast<int4*>(part + r * kRP + j0 + i) =
                             make_int4((int)v[i], (int)v[i + 1], (int)v[i + 2], (int)v[i + 3]);
                 }
-                zero_acc<BN>(d);
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&accempty[cst]);
+                if (si.more()) {   // (the CTA's last segment: no issuer waits for this accumulator again)
+                    zero_acc<BN>(d);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&accempty[cst]);
+                }
                 fence_proxy_async_smem();
                 if (et == 0) QOQ_TRACE(p, 23);
                 named_bar_sync(1, 128);
@@ -931,7 +933,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC, TP>::kBlockThreads, 1)
                 tmem_ld_chunk<BN>(d + j0, v);
                 tmem_wait_ld();
                 if (et == 0 && ci == 0) QOQ_TRACE(p, 27);
-                if (ci == BN / C::kChunk - 1) {          // accumulator fully read: zero it, hand it back
+                // accumulator fully read: zero it and hand it back, unless this is the CTA's last segment (no
+                // issuer waits for it again)
+                if (ci == BN / C::kChunk - 1 && si.more()) {
                     zero_acc<BN>(d);
                     tc_fence_before();
                     __syncwarp();
