@@ -10,30 +10,24 @@
 namespace qoq {
 
 // Block-wide max of non-negative values / int sum over a 1-D CTA (valid in every thread).
+// Block reductions with one REDUX per warp (redux.sync) and ONE barrier. Contract: each `red` array (>= 32
+// slots) is used by at most one reduction per CTA (no barrier protects its reuse). block_reduce_max takes
+// non-negative floats, whose bit patterns order like unsigned integers.
 __device__ __forceinline__ float block_reduce_max(float v, float* red) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const unsigned u = __reduce_max_sync(0xffffffffu, __float_as_uint(v));
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (l == 0) red[w] = __uint_as_float(u);
     __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    v = (l < nw) ? red[l] : 0.0f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;  // valid in every thread
+    const unsigned x = (l < nw) ? __float_as_uint(red[l]) : 0u;
+    return __uint_as_float(__reduce_max_sync(0xffffffffu, x));  // valid in every thread
 }
 
 __device__ __forceinline__ int block_reduce_sum(int v, int* red) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    v = __reduce_add_sync(0xffffffffu, v);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-    __syncthreads();
     if (l == 0) red[w] = v;
     __syncthreads();
-    v = (l < nw) ? red[l] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+    return __reduce_add_sync(0xffffffffu, (l < nw) ? red[l] : 0);
 }
 
 // Symmetric fp16 scale: fp16_rn(amax / qmax); 1.0 for amax == 0; 2^-24 if it underflows to 0.

@@ -205,28 +205,10 @@ __global__ void __launch_bounds__(128) pc_pack_kernel(const __half* __restrict__
 constexpr int kQThreads = QOQ_QTHREADS;   // (build knobs for A/B: threads per row, 16-byte vectors per thread)
 constexpr int kQVec = QOQ_QVEC;
 
-// Row reductions of the quantizer with one REDUX per warp (redux.sync): the amax is a non-negative float,
-// so its bit pattern orders like an unsigned integer. Each shared slot array is used once per row, so one
-// barrier per reduction suffices.
-__device__ __forceinline__ float row_max(float a, unsigned* red) {
-    const unsigned v = __reduce_max_sync(0xffffffffu, __float_as_uint(a));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    const unsigned w = (threadIdx.x & 31) < (blockDim.x >> 5) ? red[threadIdx.x & 31] : 0u;
-    return __uint_as_float(__reduce_max_sync(0xffffffffu, w));
-}
-__device__ __forceinline__ int row_sum(int t, int* red) {
-    const int v = __reduce_add_sync(0xffffffffu, t);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    const int w = (threadIdx.x & 31) < (blockDim.x >> 5) ? red[threadIdx.x & 31] : 0;
-    return __reduce_add_sync(0xffffffffu, w);
-}
-
 __global__ void __launch_bounds__(kQThreads) quantize_act_kernel(const __half* __restrict__ X, int K, int ldx,
                                                                  int8_t* __restrict__ qx, __half* __restrict__ sx,
                                                                  int32_t* __restrict__ tx) {
-    __shared__ unsigned redu[32];
+    __shared__ float redf[32];
     __shared__ int redi[32];
     pdl_launch_dependents();
     pdl_wait();
@@ -246,7 +228,7 @@ __global__ void __launch_bounds__(kQThreads) quantize_act_kernel(const __half* _
         __half2 a2 = __float2half2_rn(0.0f);
 #pragma unroll
         for (int j = 0; j < kQVec; ++j) a2 = amax8h(r[j], a2);
-        sh = sym_scale(row_max(amax_of(a2), redu), 127.0f);
+        sh = sym_scale(block_reduce_max(amax_of(a2), redf), 127.0f);
         const float s = __half2float(sh), inv = __frcp_rn(s);
 #pragma unroll
         for (int j = 0; j < kQVec; ++j) {
@@ -256,11 +238,11 @@ __global__ void __launch_bounds__(kQThreads) quantize_act_kernel(const __half* _
     } else {
         __half2 a2 = __float2half2_rn(0.0f);
         for (int i = threadIdx.x; i < nv; i += kQThreads) a2 = amax8h(__ldg(row + i), a2);
-        sh = sym_scale(row_max(amax_of(a2), redu), 127.0f);
+        sh = sym_scale(block_reduce_max(amax_of(a2), redf), 127.0f);
         const float s = __half2float(sh), inv = __frcp_rn(s);
         for (int i = threadIdx.x; i < nv; i += kQThreads) out[i] = quant8(__ldg(row + i), s, inv, t);
     }
-    if (tx) t = row_sum(t, redi);
+    if (tx) t = block_reduce_sum(t, redi);
     if (threadIdx.x == 0) {
         sx[m] = sh;
         if (tx) tx[m] = t;
