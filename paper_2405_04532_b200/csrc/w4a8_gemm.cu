@@ -477,7 +477,9 @@ __device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[Cfg<
 
 // TP = true: the fused TP reduction (NEXT-3) — its own instantiation, so the other kernels carry none of its
 // registers (the BN <= 64 kernels run 640 threads at the 96-register cap)
-template <int BN, bool OUT_I32, int CG, bool PC = false, bool TP = false>
+// FQ = true: qoq_w4a8_linear's one-kernel path (per-token quantization in the prologue, QOQ_LINEAR_FUSED=1) —
+// its own instantiation, so the production kernels carry none of its code
+template <int BN, bool OUT_I32, int CG, bool PC = false, bool TP = false, bool FQ = false>
 __global__ void __launch_bounds__(Cfg<BN, CG, PC, TP>::kBlockThreads, 1)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const KParams p) {
     using C = Cfg<BN, CG, PC, TP>;
@@ -600,7 +602,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC, TP>::kBlockThreads, 1)
         // ===================== activation producer: TMA 2-D (SWIZZLE_128B) k-tiles of q_x
         if (lane == 0) {
             pdl_wait();
-            if (p.X) {   // fused quantization: every CTA's q_x rows written (acquire), then visible
+            if constexpr (FQ) {   // fused quantization: every CTA's q_x rows written (acquire), then visible
                 spin_until_ge(p.qsync, (int)gridDim.x);   // to this thread's async-proxy (TMA) reads
                 fence_proxy_async_global();
                 fused_depart(p);
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC, TP>::kBlockThreads, 1)
             tp_par = gen & 1u;
             tp_flag = gen + 1u;
         }
-        if (p.X) {   // fused per-token quantization of X, then the grid handshake (s_x / t_x below)
+        if constexpr (FQ) {   // fused per-token quantization of X, then the grid handshake (s_x / t_x below)
             fused_quantize_rows(p, et, sxs, txs);
             if (et == 0) {
                 QOQ_TRACE(p, 3);
@@ -1269,10 +1271,10 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     return p;
 }
 
-template <int BN, bool OUT_I32, int CG, bool PC = false, bool TP = false>
+template <int BN, bool OUT_I32, int CG, bool PC = false, bool TP = false, bool FQ = false>
 static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t st, bool pdl) {
     using C = Cfg<BN, CG, PC, TP>;
-    auto kern = w4a8_gemm_kernel<BN, OUT_I32, CG, PC, TP>;
+    auto kern = w4a8_gemm_kernel<BN, OUT_I32, CG, PC, TP, FQ>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     auto enc = tensor_map_encoder();
@@ -1340,6 +1342,17 @@ static cudaError_t launch_bn(const GemmArgs& a, const GemmPlan& pl, cudaStream_t
 
 template <int BN>
 static cudaError_t launch_bn_cg(const GemmArgs& a, const GemmPlan& p, cudaStream_t st, bool pdl) {
+    if (a.X) {    // qoq_w4a8_linear's one-kernel path: fp16 out, M <= kFuseMaxM (token tiles 16 / 32 / 64)
+        if (a.out_i32 || a.zw || a.tp) return cudaErrorInvalidValue;
+        if constexpr (BN <= 64) {
+            if (p.CG == 2) {
+                if constexpr (BN >= 32) return launch_bn<BN, false, 2, false, false, true>(a, p, st, pdl);
+                return cudaErrorInvalidValue;
+            }
+            return launch_bn<BN, false, 1, false, false, true>(a, p, st, pdl);
+        }
+        return cudaErrorInvalidValue;
+    }
     if (a.tp) {   // fused TP reduction: whole tiles, single CTAs, fp16 out (tp_plan)
         if (p.CG != 1 || p.mode != 0 || a.out_i32 || a.zw) return cudaErrorInvalidValue;
         if constexpr (BN <= 128) return launch_bn<BN, false, 1, false, true>(a, p, st, pdl);
