@@ -9,6 +9,13 @@
 //   5  TMA 2-D tensor loads (box 128 B x 64 rows, SWIZZLE_128B, two per step) from a row-major [64][4096] q_x,
 //      as the GEMM's activation producer does
 //   6  as 5, issued by the weight producer thread itself (one TMA issuer)
+//   7  as 5, the weight copies with the GEMM's L2::cache_hint evict_first policy
+//   8  as 5, plus 4 warps reading every weight step from shared memory (LDS.128, as the dequant warps)
+//   9  as 8, plus the same 4 warps reading every activation step (as the MMA's B operand reads)
+//  10  weights NOT staged in shared memory: the producer prefetches them into L2 (cp.async.bulk.prefetch.L2,
+//      kPf steps ahead) and the 4 warps load them straight into registers (LDG.128, two steps in flight),
+//      activations by TMA as in 9 and read from shared memory
+//  11  as 10 with 3 steps of weights in flight per thread
 // Prints weight bytes per cycle per SM and the aggregate weight TB/s.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/ingress_bench2.cu -o tools/ingress_bench2
 #include <cstdio>
@@ -61,11 +68,11 @@ __global__ void __launch_bounds__(224, 1) pipe(const __grid_constant__ CUtensorM
     if (threadIdx.x == 0) {
         for (int i = 0; i < kWR; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wfull[i])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wfree[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&wfree[i])), "r"((variant == 8 || variant == 9) ? 4 : 1));
         }
         for (int i = 0; i < kXR; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&xfull[i])), "r"(variant == 3 ? 4 : 1));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&xfree[i])), "r"(C));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&xfree[i])), "r"(variant >= 9 ? 4 : C));
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
@@ -75,13 +82,21 @@ __global__ void __launch_bounds__(224, 1) pipe(const __grid_constant__ CUtensorM
     }
     const long long t0 = clock64();
     const bool acts = variant != 4;
-    if (warp == 0 && lane == 0) {            // weight producer
+    if (warp == 0 && lane == 0 && variant != 10 && variant != 11) {            // weight producer
         const uint8_t* base = w + per * blockIdx.x;
         for (int it = 0; it < kIters; ++it) {
             const int i = it % kWR;
             if (it >= kWR) wait(&wfree[i], ((it / kWR) - 1) & 1);
             expect(&wfull[i], kW);
-            bulk(sm + i * kWS, base + (size_t)it * kW, kW, &wfull[i]);
+            if (variant == 7) {
+                uint64_t pol;
+                asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                             ::"r"(smem_u32(sm + i * kWS)), "l"(base + (size_t)it * kW), "r"(kW), "r"(smem_u32(&wfull[i])),
+                             "l"(pol) : "memory");
+            } else {
+                bulk(sm + i * kWS, base + (size_t)it * kW, kW, &wfull[i]);
+            }
             if (variant == 6) {
                 const int j = it % kXR;
                 if (it >= kXR) wait(&xfree[j], ((it / kXR) - 1) & 1);
@@ -92,7 +107,7 @@ __global__ void __launch_bounds__(224, 1) pipe(const __grid_constant__ CUtensorM
                                  "r"(smem_u32(&xfull[j])) : "memory");
             }
         }
-    } else if (warp == 1 && lane == 0 && variant == 5) {   // activation producer: 2-D tensor loads
+    } else if (warp == 1 && lane == 0 && (variant == 5 || variant >= 7)) {   // activation producer: 2-D tensor loads
         for (int it = 0; it < kIters; ++it) {
             const int i = it % kXR;
             if (it >= kXR) wait(&xfree[i], ((it / kXR) - 1) & 1);
@@ -102,7 +117,7 @@ __global__ void __launch_bounds__(224, 1) pipe(const __grid_constant__ CUtensorM
                              ::"r"(smem_u32(xs + i * kX + t * 8192)), "l"(&tmx), "r"(((2 * it + t) % 32) * 128), "r"(0),
                              "r"(smem_u32(&xfull[i])) : "memory");
         }
-    } else if (warp == 1 && lane == 0 && acts && variant != 3 && variant != 6) {   // activation producer (TMA)
+    } else if (warp == 1 && lane == 0 && acts && variant != 3 && variant >= 0 && variant < 5) {   // activation producer (TMA)
         for (int it = 0; it < kIters; ++it) {
             const int i = it % kXR;
             if (it >= kXR) wait(&xfree[i], ((it / kXR) - 1) & 1);
@@ -130,7 +145,60 @@ __global__ void __launch_bounds__(224, 1) pipe(const __grid_constant__ CUtensorM
             __syncwarp();
             if (lane == 0) arrive(&xfull[i]);
         }
-    } else if (warp == 2 && lane == 0) {     // consumer
+    } else if (warp == 0 && lane == 0 && (variant == 10 || variant == 11)) {   // L2 prefetch of the weights
+        const uint8_t* base = w + per * blockIdx.x;
+        for (int it = 0; it < kIters; it += 4)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + (size_t)it * kW), "r"(4 * kW) : "memory");
+    } else if (warp >= 3 && warp < 7 && (variant == 10 || variant == 11)) {   // weights by LDG, acts from smem
+        const int t = threadIdx.x - 96;
+        const uint4* wg = reinterpret_cast<const uint4*>(w + per * blockIdx.x);
+        uint32_t acc = 0;
+        constexpr int kD = 3;
+        uint4 buf[kD][8];
+        const int D = variant == 10 ? 2 : 3;
+        for (int d = 0; d < D; ++d)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) buf[d][k] = __ldcg(wg + (size_t)d * (kW / 16) + t + 128 * k);
+        for (int it = 0; it < kIters; ++it) {
+            const int j = it % kXR, b = it % D;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc += buf[b][k].x ^ buf[b][k].w;
+            if (it + D < kIters)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) buf[b][k] = __ldcg(wg + (size_t)(it + D) * (kW / 16) + t + 128 * k);
+            wait(&xfull[j], (it / kXR) & 1);
+            const uint4* xv = reinterpret_cast<const uint4*>(xs + j * kX);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { const uint4 v = xv[t + 128 * k]; acc += v.y ^ v.z; }
+            __syncwarp();
+            if (lane == 0) arrive(&xfree[j]);
+        }
+        if (acc == 0x12345678u) cyc[0] = -1;
+    } else if (warp >= 3 && warp < 7 && (variant == 8 || variant == 9)) {   // shared-memory readers
+        const int t = threadIdx.x - 96;
+        uint32_t acc = 0;
+        for (int it = 0; it < kIters; ++it) {
+            const int i = it % kWR, j = it % kXR;
+            wait(&wfull[i], (it / kWR) & 1);
+            const uint4* ws = reinterpret_cast<const uint4*>(sm + i * kWS);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { const uint4 v = ws[t + 128 * k]; acc += v.x ^ v.w; }
+            if (variant == 9) {
+                wait(&xfull[j], (it / kXR) & 1);
+                const uint4* xv = reinterpret_cast<const uint4*>(xs + j * kX);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) { const uint4 v = xv[t + 128 * k]; acc += v.y ^ v.z; }
+            }
+            if (variant == 8 && warp == 3 && lane == 0) {   // activations consumed unread (one arrival)
+                wait(&xfull[j], (it / kXR) & 1);
+                arrive(&xfree[j]);
+            }
+            __syncwarp();
+            if (lane == 0) arrive(&wfree[i]);
+            if (variant == 9 && lane == 0) arrive(&xfree[j]);
+        }
+        if (acc == 0x12345678u) cyc[0] = -1;   // keep the loads
+    } else if (warp == 2 && lane == 0 && variant < 8) {     // consumer
         for (int it = 0; it < kIters; ++it) {
             const int i = it % kWR, j = it % kXR;
             wait(&wfull[i], (it / kWR) & 1);
@@ -162,7 +230,7 @@ int main() {
     const int smem = kWR * kWS + kXR * kX + 2048;
     cudaFuncSetAttribute(pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(pipe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    const char* names[7] = {"TMA own", "TMA mcast2", "TMA mcast4", "LSU acts", "no acts", "TMA 2-D", "2-D 1 issuer"};
+    const char* names[12] = {"TMA own", "TMA mcast2", "TMA mcast4", "LSU acts", "no acts", "TMA 2-D", "2-D 1 issuer", "2-D evict1st", "+LDS W", "+LDS W+X", "W by LDG x2", "W by LDG x3"};
     // q_x [64][4096] int8 row-major, box {128, 64}, SWIZZLE_128B (the GEMM's activation map at M = 64)
     uint8_t* qx;
     cudaMalloc(&qx, 64 * 4096);
@@ -181,7 +249,7 @@ int main() {
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     for (int G : {32, 64, 128, 148}) {
-        for (int variant : {0, 3, 4, 5, 6}) {
+        for (int variant : {9, 10, 11}) {
             const int C = variant == 1 ? 2 : variant == 2 ? 4 : 1;
             if (G % C) continue;
             long long hc[148];
@@ -214,6 +282,7 @@ int main() {
             }
             printf("G=%3d %-10s: weights %6.1f B/cycle/SM  (%.2f TB/s aggregate at 1.965 GHz; slowest CTA %.0f cycles/step)\n",
                    G, names[variant], s / G, s * 1.965e9 / 1e12, mx / kIters);
+            fflush(stdout);
         }
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
