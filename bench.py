@@ -490,6 +490,10 @@ def main():
             diff = max(float((Ybuf[n].float() - ref_rows[n].float()).abs().max()) for n in ref_rows)
             scale = max(float(ref_rows[n].float().abs().max()) for n in ref_rows)
             ok = st == 0 and diff <= 4e-3 * scale + 2e-3 * world
+            # every rank takes the same branch (the timed leg has barriers / all-reduces): ok on ALL ranks
+            okt = torch.tensor([1 if ok else 0], device=dev)
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+            ok = bool(okt.item())
             tp_fused = {"status": st, "max_abs_diff_vs_nccl_step": diff, "ok": ok}
             if ok:
                 g_fused = torch.cuda.CUDAGraph()
