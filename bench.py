@@ -377,6 +377,11 @@ def main():
                        else qoq.TpComm.local(M, n_cap, dev))
         except Exception as e:   # reported in the line; the NCCL step is the measured default
             tp_comm_err = f"{type(e).__name__}: {e}"
+        if world > 1:   # all ranks keep the leg, or none does
+            okt = torch.tensor([0 if tp_comm is None else 1], device=dev)
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+            if not okt.item() and tp_comm is not None:
+                tp_comm, tp_comm_err = None, "the fused-reduction setup failed on another rank"
 
     def make_linear(gemm_only, counter, fused_rows=False):
         def linear(X_r, shard, entry):
