@@ -67,6 +67,30 @@ def test_world1_equals_gemm_every_call(gpu_lib, M, N, K):
     assert np.all(np.abs(y - y_ref) <= RTOL * np.abs(y_ref) + ATOL)
 
 
+@pytest.mark.parametrize("M,N,K,mcap,ncap", [(37, 1280, 512, 64, 4096), (5, 256, 1792, 16, 512)])
+def test_comm_larger_than_the_call(gpu_lib, M, N, K, mcap, ncap):
+    """A comm sized for the largest call (m_cap > M, n_cap > N) serves smaller calls: the slots are pitched by
+    the caps, at world 1 and with a pre-seeded peer at world 2."""
+    cases = [_rank_inputs(M, N, K, seed=500 + r) for r in range(2)]
+    parts = [_partial(M, N, K, c) for c in cases]
+    comm1 = gpu_lib.TpComm.local(mcap, ncap, dev())
+    p, s0, qx, sx, tx = (to_dev(a) for a in cases[0])
+    for _ in range(2):
+        assert torch.equal(gpu_lib.w4a8_gemm_allreduce(qx, sx, tx, p, s0, N, comm1), parts[0])
+    recv = _rank_buffers(gpu_lib, mcap, ncap, 2)
+    comm2 = gpu_lib.TpComm(0, 2, [r.data_ptr() for r in recv], mcap, ncap, dev(), keep=(recv,))
+    want = torch.from_numpy(oracle.tp_reduce_rank_order([y.cpu().numpy() for y in parts])).to(dev())
+    for call in range(2):
+        par, flag = call & 1, call + 1
+        _words(recv[0], par, 1, mcap, ncap)[:M, : N // 2].copy_(_ll(parts[1], flag))
+        torch.cuda.synchronize()
+        Y = gpu_lib.w4a8_gemm_allreduce(qx, sx, tx, p, s0, N, comm2)
+        torch.cuda.synchronize()
+        assert comm2.status() == 0 and torch.equal(Y, want)
+        assert torch.equal(_words(recv[1], par, 0, mcap, ncap)[:M, : N // 2], _ll(parts[0], flag))
+    assert comm1.status() == 0
+
+
 def test_world1_cuda_graph_replay(gpu_lib):
     M, N, K = 64, 4096, 512
     case = _rank_inputs(M, N, K, seed=5)
