@@ -171,6 +171,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef QOQ_W_L2_PREFETCH
 #define QOQ_W_L2_PREFETCH 0   // bulk L2 prefetch of each decode segment's weights (A/B knob)
 #endif
+#ifndef QOQ_EXPAND_EARLY
+#define QOQ_EXPAND_EARLY 1   // token tiles > 64: expand a step before waiting for its TMEM buffer (+1-1.5% prefill)
+#endif
 #ifndef QOQ_W_PREFILL
 #define QOQ_W_PREFILL 1   // W-ring stages issued before the setup barrier (each issue costs ~250 cycles)
 #endif
@@ -739,6 +742,19 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC, TP>::kBlockThreads, 1)
                     if (tw) QOQ_TRACE_IT(p, it, 1);
                     const int as = it % C::kAStages;
                     const uint32_t aph = (uint32_t)(it / C::kAStages) & 1u;
+                    // (kXE: expand both k-tiles BEFORE waiting for the TMEM buffer: the ALU work overlaps the MMAs
+                    // still reading it, and only the stores wait; 512-thread tiles only, for the registers)
+                    constexpr bool kXE = QOQ_EXPAND_EARLY && BN > 64;
+                    uint32_t out2[kXE ? 2 : 1][32];
+                    if constexpr (kXE) {
+#pragma unroll
+                        for (int t = 0; t < 2; ++t) {
+                            if (t < nk && (!C::kDeqSplit || t == grp)) {
+                                if (signed_a) expand_row<true>(v[t], sc[t], bias[t], out2[t]);
+                                else expand_row<false>(v[t], sc[t], bias[t], out2[t]);
+                            }
+                        }
+                    }
                     mbar_wait(&aempty[as], aph ^ 1);             // TMEM buffer free again
                     if constexpr (CG == 2) {                     // this CTA's activation half landed
                         const int xs = it % C::kXStages;
@@ -749,11 +765,15 @@ __global__ void __launch_bounds__(Cfg<BN, CG, PC, TP>::kBlockThreads, 1)
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
                         if (t < nk && (!C::kDeqSplit || t == grp)) {
-                            uint32_t out[32];
-                            if (signed_a) expand_row<true>(v[t], sc[t], bias[t], out);
-                            else expand_row<false>(v[t], sc[t], bias[t], out);
-                            if (!(QOQ_ABLATE & 16)) tmem_st_32x32b_x32(tmem + lane_off + as * 64 + t * 32, out);
-                            else if (out[0] == 0x12345678u && out[31] == 0x9abcdef0u) asm volatile("trap;");
+                            if constexpr (kXE) {
+                                tmem_st_32x32b_x32(tmem + lane_off + as * 64 + t * 32, out2[t]);
+                            } else {
+                                uint32_t out[32];
+                                if (signed_a) expand_row<true>(v[t], sc[t], bias[t], out);
+                                else expand_row<false>(v[t], sc[t], bias[t], out);
+                                if (!(QOQ_ABLATE & 16)) tmem_st_32x32b_x32(tmem + lane_off + as * 64 + t * 32, out);
+                                else if (out[0] == 0x12345678u && out[31] == 0x9abcdef0u) asm volatile("trap;");
+                            }
                         }
                     }
                     tmem_wait_st();
