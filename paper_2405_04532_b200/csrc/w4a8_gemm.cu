@@ -1195,9 +1195,9 @@ static int max_clusters_bn(int BN, int S) {
 
 GemmPlan plan_gemm(int M, int N, int K, int num_sms) {
     GemmPlan p{};
-    // token tile: the smallest of 16/32/64/128 that holds M; above that 192 (double-buffered TMEM
-    // accumulators: the epilogue overlaps the next tile) except 192 < M <= 256, one 256-wide tile.
-    // QOQ_BN_BIG=256 forces the single-buffered 256-wide tile above M = 128 (A/B).
+    // token tile: the smallest of 16/32/64/128 that holds M; above M = 128 the cost model below picks
+    // 128, 192 (double-buffered TMEM accumulators: the epilogue overlaps the next tile) or 256 (single
+    // accumulator) by whole waves x per-tile cost, among tiles that fill the GPU.
     p.BN = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
     if (M > 128) {
         // prefill: pick the token tile by whole waves x per-tile cost, among tiles that fill the GPU

@@ -251,7 +251,7 @@ def test_tp_shards_on_device(gpu_lib):
     (40, 1280, 3200),    # BN=64: KS=13
     (64, 19200, 384),    # BN=64: 150 tiles, KS=2 with a 1-tile last step
     (100, 1280, 1664),   # BN=128: KS=7
-    (200, 768, 2688),    # BN=256: one issuer, KS=11
+    (200, 768, 2688),    # M > 128: the planner's prefill tile (BN = 128 here: 6 tiles < #SMs), KS=11
 ])
 def test_gemm_segment_edge_cases_bit_exact(gpu_lib, monkeypatch, mode, M, N, K):
     """Odd step counts, 1-tile last steps, multi-tile persistent CTAs and odd-length split-K
