@@ -2,6 +2,8 @@
 
 Bit-exact: packed weights, s0, q_x, s_x, t_x and INT32 accumulators. FP16 Y within the north_star
 tolerance |Y - y_ref| <= 2e-3 |y_ref| + 1e-3, y_ref the exact fp64 oracle value."""
+import functools
+
 import numpy as np
 import pytest
 import torch
@@ -405,3 +407,40 @@ def test_default_workspace_per_launch_stream(gpu_lib, monkeypatch):
     torch.cuda.synchronize()
     for a in outs:
         assert np.array_equal(a.cpu().numpy(), acc_ref)
+
+
+def _tp_shard_cases():
+    """BASELINE configs 4 and 5: the per-rank GEMM shapes of Llama-2-70B at TP 2 / 4 / 8 and Qwen1.5-72B at
+    TP 8 (column-parallel N / TP, row-parallel K / TP; gate and up fused), the shapes each rank's kernel runs."""
+    from paper_2405_04532_b200 import parallel
+    cases = []
+    for model, tps in (("llama2-70b", (2, 4, 8)), ("qwen1.5-72b", (8,))):
+        for tp in tps:
+            for name, Nr, Kr, N, K, kind, qg in parallel.rank_layer_plan(synth.fuse_gate_up(synth.MODELS[model][0]), tp):
+                cases.append((f"{model}-tp{tp}-{name}", Nr, Kr))
+    return cases
+
+
+@functools.lru_cache(maxsize=2)
+def _shard_weights(N, K):
+    W = synth.weights_fp16(N, K, seed=3)
+    p_ref, s0_ref = oracle.quantize_weights(W)
+    return W, p_ref, s0_ref
+
+
+@pytest.mark.parametrize("M", [1, 64, 1024])
+@pytest.mark.parametrize("case,N,K", _tp_shard_cases())
+def test_tp_shard_shapes_sampled(gpu_lib, case, N, K, M):
+    """Every rank-shard GEMM of configs 4 / 5 at decode and prefill M, in the planner's launch configuration:
+    INT32 exact and Y within tolerance on sampled token rows (first, middle, last)."""
+    W, p_ref, s0_ref = _shard_weights(N, K)
+    X = synth.activations_fp16(M, K, seed=3)
+    packed, s0 = gpu_lib.quantize_weights(to_dev(W))
+    assert np.array_equal(packed.cpu().numpy(), p_ref)
+    qx, sx, tx = gpu_lib.quantize_activations_per_token(to_dev(X))
+    Y = gpu_lib.w4a8_gemm(qx, sx, tx, packed, s0, N)
+    acc = gpu_lib.w4a8_gemm_i32(qx, tx, packed, N)
+    rows = sorted({0, M - 1, M // 2})
+    check_y(Y[rows], oracle.linear_rows(X[rows], p_ref, s0_ref, N))
+    qx_ref, _, _ = oracle.quantize_activations(X[rows])
+    assert np.array_equal(acc[rows].cpu().numpy(), oracle.acc_from_packed(qx_ref, p_ref, N, K))
