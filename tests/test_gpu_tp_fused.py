@@ -220,3 +220,17 @@ def test_fused_reduction_multi_gpu(tmp_path):
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert r.stdout.count("ok") == world
+
+
+@pytest.mark.parametrize("M", [1, 16, 64])
+@pytest.mark.parametrize("N,K", [(8192, 1024), (8192, 3584), (8192, 3072), (4096, 512), (4096, 1792)])
+def test_world1_row_parallel_shard_shapes(gpu_lib, M, N, K):
+    """The row-parallel shard shapes of configs 4 / 5 (Llama-2-70B / Qwen1.5-72B at TP 8: o, down) and of
+    Llama-3-8B at TP 8: the fused kernel (whole tiles, its own instantiation) equals the plain GEMM bit for bit."""
+    case = _rank_inputs(M, N, K, seed=7 * M + K)
+    ref = _partial(M, N, K, case)
+    p, s0, qx, sx, tx = (to_dev(a) for a in case)
+    comm = gpu_lib.TpComm.local(M, N, dev())
+    Y = gpu_lib.w4a8_gemm_allreduce(qx, sx, tx, p, s0, N, comm)
+    torch.cuda.synchronize()
+    assert comm.status() == 0 and torch.equal(Y, ref)
